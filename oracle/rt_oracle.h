@@ -1,0 +1,89 @@
+/* rt_oracle.h — TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, single-threaded CPU oracle of the random-tree Monte Carlo
+ * estimator of arXiv:2402.06491 (Acebrón & Rodríguez-Rozas), Strategy A
+ * (PAPER.md:159-301), with order binning and [L/M] Padé resummation
+ * (PAPER.md:295-301, 744-780).  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load it.  It shares no
+ * code, header, table or constant generator with the CUDA product
+ * (paper_2402_06491_b200/), and the product never loads it.
+ *
+ * Every function states the passage it follows; the numerical contract
+ * (the readings of the paper where it is silent) is DESIGN.md §2.
+ */
+#ifndef RT_ORACLE_H
+#define RT_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int32_t dim;          /* 1..3 */
+  double  D;            /* u_t = D Δu + f(u) */
+  int32_t degree;       /* m */
+  double  b[9];         /* f(u) = Σ_k b[k] u^k */
+  double  lambda;       /* clock rate; <= 0 -> default */
+  int32_t offspring;    /* 0: p_k ∝ |a_k|, 1: uniform on the support */
+  int32_t init_kind;    /* 0 const, 1 tanh step, 2 gauss, 3 lorentz */
+  double  init_amp;
+  double  init_scale;
+  int32_t K;            /* orders 0..K kept */
+  int32_t precision;    /* ignored by the oracle (FP64 throughout) */
+} or_params;
+
+typedef struct {
+  double   lambda, inv_lambda, sigma;
+  double   a[9];
+  int32_t  n_support;
+  int32_t  support[9];     /* k values, ascending */
+  uint64_t thresh[9];      /* integer thresholds T_k (last = 2^32) */
+  double   p_hat[9];       /* effective probabilities */
+  double   w[9];           /* weights a_k / (λ p̂_k) */
+  int32_t  beta;           /* bits per child digit in labels */
+} or_norm;
+
+typedef struct {
+  int32_t ne;         /* splitting events (order bin) */
+  int32_t leaves;     /* g evaluations */
+  int32_t particles;  /* particles processed */
+  int32_t pruned;     /* 1 if Ne > K (aborted) */
+  double  C;          /* tree contribution (0 if pruned) */
+} or_tree_rec;
+
+typedef struct { int64_t trees, pruned, particles, leaves, splits; } or_stats;
+
+/* Philox4x32-10 block: out = philox(key, ctr). */
+void or_philox(const uint32_t key[2], const uint32_t ctr[4], uint32_t out[4]);
+/* (2*(x>>12)+1) * 2^-53 */
+double or_unif53(uint32_t lo, uint32_t hi);
+
+int or_normalize(const or_params* p, or_norm* out);   /* 0 ok, else error */
+
+/* One tree at node x (node index i), tree index j. */
+int or_tree(const or_params* p, const double* x, int64_t i, int64_t j, double t,
+            uint64_t seed, or_tree_rec* rec);
+
+/* Records for trees j in [j0, j0+n_trees) of every node: rec[i*n_trees + (j-j0)]. */
+int or_trees(const or_params* p, const double* points, int64_t n_points, double t,
+             int64_t j0, int64_t n_trees, uint64_t seed, or_tree_rec* rec);
+
+/* Order-binned sums sums[(i*(K+2)+n)*3 + {0:ΣC, 1:ΣC², 2:count}] for n = 0..K+1
+ * (n = K+1 counts pruned trees), over trees j in [j0, j0+n_trees). */
+int or_sums(const or_params* p, const double* points, int64_t n_points, double t,
+            int64_t j0, int64_t n_trees, uint64_t seed, double* sums, or_stats* st);
+
+/* Per-order coefficients and standard errors from sums (N = total trees). */
+void or_finalize(const double* sums, int64_t n_points, int32_t K, int64_t N,
+                 double* coeffs, double* stderr_n, double* u_sum, double* se_sum);
+
+/* [L/M] Padé of c[0..L+M] evaluated at z = 1; flags bit0 zero pivot,
+ * bit1 |Q(1)| <= 1e-14 |P(1)|, bit2 Q changes sign on (0,1]. */
+int or_pade(const double* c, int32_t L, int32_t M, double* u, uint32_t* flags,
+            double* p_out, double* q_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

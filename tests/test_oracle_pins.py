@@ -1,0 +1,275 @@
+"""Pins of the oracle's estimator against mathematics other than itself.
+
+Each test names the closed form / law it uses; a plausible mistake in the
+oracle (a dropped weight, a wrong sign, σ = sqrt(D) instead of sqrt(2D), a
+transposed threshold, an off-by-one order bin, a wrong divisor) fails at least
+one of them:
+
+  weights / signs / offspring law   -> test_ode_orders_* (signed cfg2 weights),
+                                       test_uniform_rule_weights (paper P:222)
+  σ and the Brownian step           -> test_heat_kernel (D = 0.5 and 1, d = 1..3)
+  order bins / k = 1 offspring      -> test_poisson_bins, test_yule_law
+  pruning                           -> test_prune_probability
+  g at the leaves                   -> test_fd_* (tanh / Gaussian data, PDE FD)
+  divisor N incl. pruned, stderr    -> test_kpp_constant_closed_form, test_stderr_scaling
+"""
+import math
+
+import numpy as np
+import pytest
+from scipy import stats
+
+import closed_forms as cf
+import workloads as W
+
+Z = 4.0   # BASELINE.json north_star: "within 4 standard errors"
+
+
+def _eq(**kw):
+    base = dict(dim=1, D=1.0, degree=2, b=[0.0, -1.0, 1.0] + [0.0] * 6, lam=0.0,
+                offspring=0, init_kind=0, init_amp=0.3, init_scale=1.0, K=12)
+    base.update(kw)
+    b = list(base["b"]) + [0.0] * (9 - len(base["b"]))
+    base["b"] = b[:9]
+    return base
+
+
+def _pool(obs, expct, min_e=20.0):
+    """Pool cells with expected count < min_e into one (chi-square validity)."""
+    keep = expct > min_e
+    o, e = list(obs[keep]), list(expct[keep])
+    if (~keep).any() and expct[~keep].sum() > 0:
+        o.append(obs[~keep].sum()); e.append(expct[~keep].sum())
+    o, e = np.array(o, dtype=np.float64), np.array(e)
+    return o, e * o.sum() / e.sum()
+
+
+def test_kpp_is_mckean(orc):
+    """cfg1 (u_t = u_xx + u^2 - u) normalises to McKean's binary
+    branching with unit weight (Eq. prod-McK)."""
+    nz = orc.normalize(W.get("cfg1")["eq"])
+    assert nz["lam"] == 1.0 and nz["support"] == [2] and nz["w"] == [1.0]
+    assert nz["sigma"] == math.sqrt(2.0)
+
+
+def test_uniform_rule_weights(orc):
+    """Paper's offspring rule: α uniform on the support with
+    c'_α = (m-1) c_α, i.e. w = n_support * a_k / λ."""
+    eq = dict(W.get("cfg2")["eq"], offspring=W.OFFSPRING_UNIFORM)
+    nz = orc.normalize(eq)
+    assert nz["support"] == [2, 3, 4]
+    np.testing.assert_allclose(nz["w"], [3 * 0.5, 3 * 0.8, 3 * -0.3], rtol=1e-9)
+
+
+def test_kpp_constant_closed_form(orc):
+    """BASELINE.json configs[0]: constant u0 = 0.3 -> u = u0/(u0+(1-u0)e^t)
+    = 0.20631248967548748 at t = 0.5; per order c_n = c0 r^n with
+    c0 = u0 e^{-t}, r = u0 (1 - e^{-t}) (geometric series of the same ODE)."""
+    cfg = W.get("cfg1_const")
+    N = 100_000
+    c, se, us, ses, st = orc.estimate(cfg["eq"], W.nodes(cfg)[:4], cfg["t"], N, seed=0)
+    exact = cf.kpp_const(0.3, 0.5)
+    assert abs(exact - 0.20631248967548748) < 1e-15
+    assert np.all(np.abs(us - exact) < Z * ses)
+    c0, r = 0.3 * math.exp(-0.5), 0.3 * (1 - math.exp(-0.5))
+    for n in range(6):
+        assert np.all(np.abs(c[:, n] - c0 * r ** n) < Z * se[:, n] + 1e-300), n
+    assert st["trees"] == 4 * N
+
+
+@pytest.mark.parametrize("name,u0,K", [("cfg2", 0.4, 12), ("cfg4", 0.5, 16)])
+def test_ode_orders_constant_data(orc, name, u0, K):
+    """Per-order coefficients for constant data equal the z^n coefficients of
+    U' = -λU + z Σ a_k U^k (scipy DOP853), and the total equals u' = f(u)."""
+    cfg = W.get(name)
+    eq = dict(cfg["eq"], init_kind=W.G_CONST, init_amp=u0, K=K)
+    t = cfg["t"]
+    N = 60_000
+    pts = np.zeros((2, eq["dim"]))
+    c, se, us, ses, st = orc.estimate(eq, pts, t, N, seed=3)
+    a = [eq["b"][k] + (1.0 if k == 1 else 0.0) for k in range(9)]
+    ex = cf.ode_orders(a, 1.0, u0, t, K)
+    for n in range(K + 1):
+        ok = np.abs(c[:, n] - ex[n]) <= 4.5 * se[:, n] + 1e-12 * abs(ex[n])
+        assert np.all(ok | (se[:, n] == 0) & (ex[n] < 1e-4)), (n, c[:, n], ex[n], se[:, n])
+    # total through Padé: MC coefficients resummed vs the ODE solution
+    u_ode = cf.ode_u(eq["b"], u0, t)
+    L, M = cfg["L"], cfg["M"]
+    for i in range(2):
+        u, fl, _, _ = orc.pade(c[i], L, M)
+        assert abs(u - u_ode) < Z * ses[i], (u, u_ode, ses[i])
+
+
+def test_ode_orders_uniform_rule(orc):
+    """Same pin under the paper's uniform offspring rule: the expectation
+    is rule-independent (R2)."""
+    cfg = W.get("cfg2")
+    eq = dict(cfg["eq"], init_kind=W.G_CONST, init_amp=0.4, offspring=W.OFFSPRING_UNIFORM)
+    c, se, us, ses, st = orc.estimate(eq, np.zeros((1, 1)), 1.0, 80_000, seed=4)
+    a = [eq["b"][k] + (1.0 if k == 1 else 0.0) for k in range(9)]
+    ex = cf.ode_orders(a, 1.0, 0.4, 1.0, 12)
+    for n in range(6):
+        assert abs(c[0, n] - ex[n]) < 4.5 * se[0, n], n
+
+
+@pytest.mark.parametrize("dim,D", [(1, 1.0), (1, 0.5), (2, 1.0), (3, 0.5)])
+def test_heat_kernel(orc, dim, D):
+    """Linear f = -u: u = e^{-t} A (1+4Dt)^{-d/2} exp(-|x|²/(1+4Dt)) for
+    g = A e^{-|x|²} (Green's function).  Empty support: all
+    mass in order 0; a clock ring kills the tree (bin 1 holds C = 0)."""
+    eq = _eq(dim=dim, D=D, degree=1, b=[0.0, -1.0], init_kind=W.G_GAUSS, init_amp=0.4, K=3)
+    pts = W.random_nodes(4, dim, seed=dim)
+    pts[0] = 0.0
+    t, N = 1.0, 100_000
+    c, se, us, ses, st = orc.estimate(eq, pts, t, N, seed=7)
+    ex = cf.heat(pts, t, D, 1.0, 0.4)
+    assert np.all(np.abs(c[:, 0] - ex) < Z * se[:, 0])
+    assert np.all(c[:, 1:] == 0.0)
+    if dim == 1 and D == 1.0:
+        assert abs(ex[0] - 0.065808275038718392) < 1e-15
+
+
+def test_heat_kernel_tanh_data(orc):
+    """cfg1's data 0.5(1+tanh x) under f = -u: e^{-t} ∫ g(x+sqrt(2t) z) φ(z) dz
+    (Gauss–Hermite).  At x = 0, t = 0.5 this is 0.5 e^{-0.5} by symmetry."""
+    eq = _eq(degree=1, b=[0.0, -1.0], init_kind=W.G_TANH_STEP, init_amp=1.0, K=3)
+    pts = np.array([[0.0], [1.0], [-1.5]])
+    c, se, *_ = orc.estimate(eq, pts, 0.5, 100_000, seed=8)
+    g = lambda x: 0.5 * (1 + np.tanh(x))
+    for i, x in enumerate(pts[:, 0]):
+        ex = cf.heat_1d_quadrature(g, x, 0.5, 1.0, 1.0)
+        assert abs(c[i, 0] - ex) < Z * se[i, 0]
+    assert abs(cf.heat_1d_quadrature(g, 0.0, 0.5, 1.0, 1.0) - 0.5 * math.exp(-0.5)) < 1e-14
+
+
+def test_poisson_bins(orc):
+    """f = -0.5u with λ overridden to 1: a_1 = 0.5, a k = 1 offspring of weight
+    0.5.  Rings form a Poisson(t) process along one Brownian path, so
+    c_n = e^{-t} (0.5 t)^n / n! x heat(x, t) (heat without decay)."""
+    eq = _eq(degree=1, b=[0.0, -0.5], lam=1.0, init_kind=W.G_GAUSS, init_amp=0.4, K=8)
+    nz = orc.normalize(eq)
+    assert nz["support"] == [1] and nz["w"] == [0.5]
+    t, N = 1.0, 200_000
+    pts = np.array([[0.0], [0.7]])
+    c, se, us, ses, st = orc.estimate(eq, pts, t, N, seed=9)
+    h = cf.heat(pts, t, 1.0, 0.0, 0.4)
+    for n in range(5):
+        ex = math.exp(-t) * (0.5 * t) ** n / math.factorial(n) * h
+        assert np.all(np.abs(c[:, n] - ex) < Z * se[:, n]), n
+    # total = e^{-0.5 t} heat; with the default λ = 0.5 the support is empty
+    assert np.all(np.abs(us - math.exp(-0.5 * t) * h) < Z * ses)
+    eq2 = dict(eq, lam=0.0)
+    assert orc.normalize(eq2)["support"] == []
+    c2, se2, *_ = orc.estimate(eq2, pts, t, N, seed=9)
+    assert np.all(np.abs(c2[:, 0] - math.exp(-0.5 * t) * h) < Z * se2[:, 0])
+
+
+def test_yule_law(orc):
+    """Binary splitting at rate 1 (cfg1): P(Ne = n) = e^{-t} (1 - e^{-t})^n
+    (Yule process); chi-square on the order-bin counts."""
+    cfg = W.get("cfg1")
+    N = 200_000
+    s, st = orc.sums(cfg["eq"], W.nodes(cfg)[:1], 1.0, N, seed=1)
+    cnt = s[0, :, 2]
+    q = 1 - math.exp(-1.0)
+    p = np.array([math.exp(-1.0) * q ** n for n in range(cfg["eq"]["K"] + 1)])
+    p = np.append(p, 1 - p.sum())          # pruned bin
+    assert stats.chisquare(*_pool(cnt, p * N)).pvalue > 1e-3
+    assert cnt.sum() == N
+
+
+def test_tree_law_general(orc):
+    """Order law of the cfg2 equation's trees: P(Ne = n) is the z^n coefficient
+    of U' = -U + z Σ p_k U^k, U(0) = 1 (the same ODE with a_k -> λ p_k and
+    g -> 1), with p_k = |a_k| / Σ|a| from the configuration itself."""
+    cfg = W.get("cfg2")
+    N = 100_000
+    s, st = orc.sums(cfg["eq"], np.zeros((1, 1)), 1.0, N, seed=2)
+    a = np.array([0, 0, 0.5, 0.8, -0.3])
+    p = np.abs(a) / np.abs(a).sum()
+    law = cf.ode_orders(list(p), 1.0, 1.0, 1.0, 12)
+    probs = np.append(law, 1 - law.sum())
+    cnt = s[0, :, 2]
+    assert stats.chisquare(*_pool(cnt, probs * N)).pvalue > 1e-3
+
+
+def test_mean_leaves(orc):
+    """E[#leaves] = e^{λ (m̄ - 1) t} for an unpruned tree (m̄ = mean offspring):
+    binary (m̄ = 2) and the cfg2 law (m̄ = 2.875) at small t with K large."""
+    N = 100_000
+    for b, mbar, t, K in (([0.0, -1.0, 1.0], 2.0, 1.0, 40),
+                          ([0.0, -1.0, 0.5, 0.8, -0.3], 2.875, 0.4, 24)):
+        eq = _eq(degree=len(b) - 1, b=b, K=K)
+        rec = orc.trees(eq, np.zeros((1, 1)), t, N, seed=21)[0]
+        assert rec["pruned"].sum() == 0
+        lv = rec["leaves"].astype(np.float64)
+        assert abs(lv.mean() - math.exp((mbar - 1) * t)) < Z * lv.std() / math.sqrt(N)
+        assert np.all(rec["particles"] == rec["leaves"] + rec["ne"])
+
+
+def test_prune_probability(orc):
+    """Binary trees are aborted iff Ne > K: P = (1 - e^{-t})^{K+1} (Yule tail);
+    pruned trees enter no bin but count in N."""
+    eq = _eq(K=2)
+    N = 100_000
+    s, st = orc.sums(eq, np.zeros((1, 1)), 1.0, N, seed=3)
+    p = (1 - math.exp(-1.0)) ** 3
+    pr = s[0, 3, 2]
+    assert abs(pr - p * N) < Z * math.sqrt(N * p * (1 - p))
+    assert s[0, 3, 0] == 0.0 and s[0, 3, 1] == 0.0
+    assert st["pruned"] == pr and s[0, :, 2].sum() == N
+
+
+@pytest.mark.parametrize("name,xs", [("cfg1", [-2.0, 0.0, 2.0]), ("cfg2", [0.0, 1.0, -3.0])])
+def test_fd_spatial(orc, name, xs):
+    """Spatial nonlinear pin: the paper's own validation route, an implicit FD
+    solve on a fine mesh; Padé [L/M] of the MC series and
+    the plain partial sum both within 4 s.e. of FD."""
+    cfg = W.get(name)
+    eq = cfg["eq"]
+    N = 100_000
+    pts = np.array(xs).reshape(-1, 1)
+    c, se, us, ses, st = orc.estimate(eq, pts, cfg["t"], N, seed=cfg["seed"])
+    if name == "cfg1":
+        g = lambda x: 0.5 * (1 + np.tanh(x))
+    else:
+        g = lambda x: 0.4 * np.exp(-x * x)
+    ref = cf.fd_at(eq["b"][: eq["degree"] + 1], g, cfg["t"], xs)
+    for i in range(len(xs)):
+        u, fl, _, _ = orc.pade(c[i], cfg["L"], cfg["M"])
+        assert abs(u - ref[i]) < Z * ses[i], (xs[i], u, ref[i], ses[i])
+        assert abs(us[i] - ref[i]) < Z * ses[i]
+
+
+def test_fd_reference_anchors():
+    """The FD reference itself: grid refinement changes it by < 2e-6."""
+    g = lambda x: 0.5 * (1 + np.tanh(x))
+    a = cf.fd_at((0, -1, 1), g, 0.5, [-2.0, 0.0, 2.0])
+    b = cf.fd_at((0, -1, 1), g, 0.5, [-2.0, 0.0, 2.0], dx=0.01, dt=1e-3)
+    assert np.max(np.abs(a - b)) < 2e-6
+
+
+def test_stderr_scaling(orc):
+    """Quadrupling N halves the standard error within 20 %."""
+    cfg = W.get("cfg2")
+    pts = np.array([[0.0]])
+    _, _, _, s1, _ = orc.estimate(cfg["eq"], pts, 1.0, 20_000, seed=1)
+    _, _, _, s4, _ = orc.estimate(cfg["eq"], pts, 1.0, 80_000, seed=1)
+    assert 0.4 < s4[0] / s1[0] < 0.6
+
+
+def test_prefix_and_offsets(orc):
+    """Counter-based draws: tree j is the same whatever range it is computed in
+    (prefix property), and range sums add up."""
+    cfg = W.get("cfg2")
+    pts = W.nodes(cfg)[30:32]
+    a = orc.trees(cfg["eq"], pts, 1.0, 300, seed=5)
+    b = orc.trees(cfg["eq"], pts, 1.0, 100, seed=5, j0=200)
+    assert np.array_equal(a[:, 200:], b)
+    s_all, _ = orc.sums(cfg["eq"], pts, 1.0, 300, seed=5)
+    s1, _ = orc.sums(cfg["eq"], pts, 1.0, 120, seed=5)
+    s2, _ = orc.sums(cfg["eq"], pts, 1.0, 180, seed=5, j0=120)
+    np.testing.assert_allclose(s1 + s2, s_all, rtol=1e-13, atol=1e-300)
+    # a different seed gives different trees
+    c = orc.trees(cfg["eq"], pts, 1.0, 300, seed=6)
+    assert not np.array_equal(a["C"], c["C"])
