@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path (BASELINE.json metric: random trees/s and
+leaf-evals/s on 1 B200; % of the FP64 issue roofline).
+
+A step = one pass of every §8(a) row over the workload: tree walk with
+order-binned reduction (rt_sums_dev), [merge across ranks], finalisation
+(rt_finalize_dev) and per-node [L/M] Padé (rt_pade_dev).  Default workload:
+cfg4 (BASELINE.json configs[3]: 1024 nodes on the planes x=0, y=0, z=0 of
+[-2,2]^3, 1e7 trees/node, d = 3, t = 1, K = 16, [7/7]) — the configuration the
+north star's roofline target is stated on.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4|cfg2|cfg3|cfg1]
+    python bench.py --impl reference ...   # the CPU oracle on the same config
+
+Multi-GPU (torchrun): weak scaling; rank r samples trees [r*N, (r+1)*N) of
+every node, the per-node sums are merged with one all-reduce (0.4 MB).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+# FP64 pipe: 64 lanes/clk/SM on B200 (sm_100), 148 SMs, 1965 MHz max clock
+# (MEASURED_PEAKS.json sm_max_mhz; /opt/skills/guides/B200_PROFILING.md).
+N_SM, FP64_LANES, F_MAX_MHZ = 148, 64, 1965.0
+
+# Algorithmic FP64 lane-instructions per operation of the method (DESIGN.md
+# §5): the FP64 instructions CUDA's own libdevice routines issue on their
+# fast path (SASS counts of DFMA/DMUL/DADD/DSETP/DMNMX/F2F.F64 per call),
+# plus the method's plain arithmetic.
+COST = dict(log=26, sqrt=9, sincospi=28, cospi=17, exp=19, tanh=27, rcp_div=9, unif=1)
+
+
+def algo_fp64_ops(eq: dict, stats: dict) -> float:
+    """Algorithmic FP64 lane-ops of one launch from its event counters."""
+    d = eq["dim"]
+    parts, leaves, splits, trees = stats["particles"], stats["leaves"], stats["splits"], stats["trees"]
+    # per particle: U_S (unif + log + mul), compare, Box–Muller pair(s)
+    # (2 unif, log, mul, sqrt, sincospi, 2 mul), sqrt(h), sigma*sqrt, d FMA
+    bm_pairs = 1 if d <= 2 else 2
+    per_particle = (COST["unif"] + COST["log"] + 1 + 1 +
+                    bm_pairs * (2 * COST["unif"] + COST["log"] + 1 + COST["sqrt"] + 2)
+                    + (COST["sincospi"] if True else 0) + (COST["cospi"] if d == 3 else 0)
+                    + COST["sqrt"] + 1 + d)
+    g = {W.G_CONST: 0, W.G_TANH_STEP: COST["tanh"] + 3, W.G_GAUSS: COST["exp"] + 2 + 2 * (d - 1),
+         W.G_LORENTZ: COST["rcp_div"] + 2 + 2 * (d - 1)}[eq["init_kind"]]
+    per_leaf = g + 1
+    per_split = 2          # Π *= w_k, τ − S
+    per_tree = 2           # ΣC += C, ΣC² = fma(C, C, ΣC²)
+    return parts * per_particle + leaves * per_leaf + splits * per_split + trees * per_tree
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+
+    def summary(self) -> dict:
+        rows = [r.split(",") for r in getattr(self, "out", "").strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                s = float(r[1]); mx = max(mx, float(r[2])); p = float(r[3])
+            except (ValueError, IndexError):
+                continue
+            if p > 200.0:                          # under load
+                sm.append(s)
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(rows), "samples_under_load": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def oracle_sample(cfg: dict, budget_s: float):
+    """Time the oracle as it stands (single-threaded) on a bounded sample of the
+    workload: the first nodes x first trees, sized to about budget_s."""
+    import oracle
+    oracle.build()
+    eq, t = cfg["eq"], cfg["t"]
+    pts = W.nodes(cfg)
+    t0 = time.perf_counter()
+    _, st = oracle.sums(eq, pts[:1], t, 2000, seed=cfg["seed"])
+    per_tree = (time.perf_counter() - t0) / 2000
+    n_nodes = min(len(pts), 16)
+    n_trees = max(64, int(budget_s / per_tree / n_nodes))
+    t0 = time.perf_counter()
+    _, st = oracle.sums(eq, pts[:n_nodes], t, n_trees, seed=cfg["seed"])
+    dt = time.perf_counter() - t0
+    return dict(seconds=dt, trees=st["trees"], leaves=st["leaves"], particles=st["particles"],
+                sample=f"{n_nodes} nodes x {n_trees} trees of {cfg['name']} (first nodes, first trees)")
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    budget = float(os.environ.get("RT_REF_STEP_S", "4.0"))
+    times, trees, leaves = [], 0, 0
+    for s in range(args.warmup + args.steps):
+        r = oracle_sample(cfg, budget)
+        if s >= args.warmup:
+            times.append(r["seconds"]); trees += r["trees"]; leaves += r["leaves"]
+            sample = r["sample"]
+    tot = sum(times)
+    v = trees / tot
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "trees/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config_json(cfg, ws),
+            "leaf_evals_per_s": leaves / tot,
+            "cpu_baseline": {"value": v, "unit": "trees/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "trees/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "random trees/sec and leaf-evals/sec on 1 B200; % of FP64 issue roofline"
+
+
+def _config_json(cfg, ws):
+    eq = cfg["eq"]
+    return {"workload": cfg["name"], "nodes": int(len(W.nodes(cfg))), "trees_per_node": cfg["n_trees"],
+            "dim": eq["dim"], "t": cfg["t"], "K": eq["K"], "pade": f"[{cfg['L']}/{cfg['M']}]",
+            "b": eq["b"][: eq["degree"] + 1], "g": ["const", "tanh_step", "gauss", "lorentz"][eq["init_kind"]],
+            "parallelism": f"trees sharded over {ws} GPU(s)" if ws > 1 else "1 GPU",
+            "l2": "256 MiB buffer written between timed steps (inputs are KB-sized)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--trees", type=int, default=0, help="override trees per node")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = W.get(args.config)
+    cfg["name"] = args.config
+    if args.trees:
+        cfg["n_trees"] = args.trees
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import paper_2402_06491_b200 as P
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    eq, t, N, seed = cfg["eq"], cfg["t"], cfg["n_trees"], cfg["seed"]
+    K, L, M = eq["K"], cfg["L"], cfg["M"]
+    pts = W.nodes(cfg)
+    n = len(pts)
+    x = torch.as_tensor(pts, device="cuda")
+    est = P.Estimator(eq)
+    sums = torch.empty((n, K + 2, 3), dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        est.sums(x, t, N, seed, tree_offset=rank * N, out=sums)
+        if dist is not None:
+            dist.all_reduce(sums)
+        c, se, us, ses = P.finalize(sums, K, N * ws)
+        u, fl = P.pade(c, L, M)
+        return u, ses
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st_one = est.stats()            # counters of one launch (same every step)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    walk_ms = []
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            flush.fill_(s)                        # evict L2 between timed steps
+            ev[s][0].record(stream)
+            u, ses = step()
+            ev[s][1].record(stream)
+            walk_ms.append(est.stats()["kernel_ms"])   # tree-walk launch, events on its stream
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(step_ms)
+    walk_avg = sum(walk_ms) / len(walk_ms)
+    if dist is not None:
+        tt = torch.tensor([tot_ms, walk_avg], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tot_ms, walk_avg = tt.tolist()
+    trees_all = n * N * ws * args.steps
+    value = trees_all / (tot_ms / 1e3)
+    leaves_all = st_one["leaves"] * ws * args.steps
+    ops = algo_fp64_ops(eq, st_one)
+    peak = N_SM * FP64_LANES * F_MAX_MHZ * 1e6 / 1e12       # T lane-ops/s
+    achieved = ops / (walk_avg / 1e3) / 1e12
+    clocks = clk.summary()
+
+    # ---- end to end through the public host API (rt_interface_values) -----
+    e2e = None
+    if cfg["nodes"]["kind"] == "planes":
+        planes = cfg["nodes"]["planes"]
+        est.interface_values(planes, n, t, N, seed, L, M)          # warm
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_steps = max(1, min(args.steps, 3))
+        for _ in range(e2e_steps):
+            est.interface_values(planes, n, t, N, seed, L, M)
+        e2e_s = time.perf_counter() - t0
+        if dist is not None:
+            tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = tt.item()
+        e2e = {"value": n * N * ws * e2e_steps / e2e_s, "unit": "trees/s",
+               "h2d_bytes_per_step": n * eq["dim"] * 8,
+               "d2h_bytes_per_step": n * eq["dim"] * 8 + n * 8 * 2 + n * 4,
+               "api": "rt_interface_values (host buffers; node placement, walk, Padé, copies)"}
+    else:
+        pin = torch.as_tensor(pts).pin_memory()
+        oc = torch.empty((n, K + 1), dtype=torch.float64).pin_memory()
+        os_ = torch.empty_like(oc).pin_memory()
+        est.estimate_host(pin, t, N, seed, oc, os_)
+        t0 = time.perf_counter()
+        for _ in range(max(1, min(args.steps, 3))):
+            est.estimate_host(pin, t, N, seed, oc, os_)
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": n * N * max(1, min(args.steps, 3)) / e2e_s, "unit": "trees/s",
+               "h2d_bytes_per_step": pin.numel() * 8, "d2h_bytes_per_step": 2 * oc.numel() * 8,
+               "api": "rt_estimate (pinned host buffers)"}
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return 0
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        r = oracle_sample(cfg, float(os.environ.get("RT_CPU_BASELINE_S", "15")))
+        cpu = {"value": r["trees"] / r["seconds"], "unit": "trees/s", "cores": 1, "kind": "oracle",
+               "sample": r["sample"], "leaf_evals_per_s": r["leaves"] / r["seconds"]}
+    line = {
+        "metric": METRIC, "value": value, "unit": "trees/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config_json(cfg, ws),
+        "leaf_evals_per_s": leaves_all / (tot_ms / 1e3),
+        "particles_per_s": st_one["particles"] * ws * args.steps / (tot_ms / 1e3),
+        "pruned_fraction": st_one["pruned"] / max(1, st_one["trees"]),
+        "roofline": {"bound": "alu", "kernel": "tree_walk_kernel", "achieved": achieved,
+                     "peak": peak, "unit": "T FP64 lane-ops/s", "frac": achieved / peak,
+                     "traffic": None, "launch_ms": walk_avg,
+                     "algorithmic_fp64_ops_per_launch": ops,
+                     "peak_basis": "148 SM x 64 FP64 lanes/clk x 1965 MHz (B200_PROFILING.md nominal; MEASURED_PEAKS.json has no FP64 entry)",
+                     "frac_at_measured_clock": (achieved / (N_SM * FP64_LANES * clocks["sm_mhz"] * 1e6 / 1e12)
+                                                if clocks.get("sm_mhz") else None)},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "clocks": clocks,
+        "gpu_launches": 4 * args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

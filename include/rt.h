@@ -1,0 +1,207 @@
+/* rt.h — C ABI of the B200 (sm_100a) random-tree Monte Carlo library.
+ *
+ * The library estimates u(x,t) for the semilinear parabolic Cauchy problem
+ *
+ *     u_t = D Δu + f(u),  x ∈ R^d,  u(x,0) = g(x),  f(u) = Σ_{k=0}^{m} b_k u^k
+ *
+ * (arXiv:2402.06491, Eq. nonlinear_new, constant-coefficient
+ * case) at a set of nodes, e.g. the interface nodes of a probabilistic domain
+ * decomposition.  Each Monte Carlo sample is a generalized
+ * random tree (Strategy A): particles live for exponential
+ * times, branch into k offspring with weight a_k/(λ p_k), move by Brownian
+ * increments, and the tree contributes the product of g over its leaves times
+ * its weights (Eq. rep_strategyB), binned by its number of
+ * splitting events Ne (Eq. recursion).  The per-order series
+ * is resummed per node by an [L/M] Padé approximant at z = 1
+ * (PAPER.md:295-301, 744-780).  The numerical contract (RNG layout, order
+ * bins, prune rule, standard errors, Padé flags) is DESIGN.md §2.
+ *
+ * Conventions for every entry point:
+ *   - Return value: rt_status; RT_OK = 0.  On failure rt_last_error() returns
+ *     a thread-local, NUL-terminated message (valid until the next call on the
+ *     same thread).  Output buffers are unspecified after a failure.
+ *   - The caller owns every input and output buffer.  rt_create copies the
+ *     parameters; the handle owns its device scratch (grown lazily, freed by
+ *     rt_destroy).  A handle must not be used from two threads at once.
+ *   - "host" pointers are ordinary CPU memory; such calls are synchronous.
+ *     "_dev" entry points take device pointers and a cudaStream_t (as void*;
+ *     NULL = legacy default stream), are stream-ordered and do not
+ *     synchronize.
+ *   - Layouts are row-major, FP64 unless stated: points [n_points × dim];
+ *     coefficients / standard errors [n_points × (K+1)].
+ *   - Results are a pure function of (parameters, points, t, tree range,
+ *     seed) and the launch geometry; with a fixed geometry they are bitwise
+ *     reproducible run to run, and tree j of node i is the same tree whatever
+ *     range or geometry computes it (counter-based RNG).
+ */
+#ifndef RT_H
+#define RT_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RT_OK = 0,
+  RT_E_ARG = 1,     /* invalid argument (null pointer, out-of-range value) */
+  RT_E_CUDA = 2,    /* CUDA runtime error (message in rt_last_error)        */
+  RT_E_NOMEM = 3,   /* device allocation failed                            */
+  RT_E_STATE = 4    /* handle state error                                  */
+} rt_status;
+
+/* Offspring law for the branching power α. */
+typedef enum {
+  RT_OFFSPRING_ABS = 0,     /* p_k ∝ |a_k| on the support (R2, default) */
+  RT_OFFSPRING_UNIFORM = 1  /* uniform on the support, the paper's rule P:222     */
+} rt_offspring;
+
+/* Initial data g (u(x,0) = g(x)). */
+typedef enum {
+  RT_G_CONST = 0,      /* g = amp                                   */
+  RT_G_TANH_STEP = 1,  /* g = amp * 0.5 * (1 + tanh(x_1 / scale))   */
+  RT_G_GAUSS = 2,      /* g = amp * exp(-|x|^2 / scale^2)           */
+  RT_G_LORENTZ = 3     /* g = amp / (1 + |x|^2 / scale^2)           */
+} rt_init;
+
+typedef enum {
+  RT_PREC_FP64 = 0,       /* everything FP64                                     */
+  RT_PREC_FP32_POS = 1    /* reserved: FP32 positions / FP64 accumulation (cfg5) */
+} rt_precision;
+
+typedef struct {
+  int32_t dim;          /* d ∈ {1,2,3}                                             */
+  double  D;            /* diffusion > 0; Brownian σ = sqrt(2D) (R5)     */
+  int32_t degree;       /* m ∈ [0, 8]                                              */
+  double  b[9];         /* f(u) = Σ_{k=0}^{m} b[k] u^k; b[k>m] ignored             */
+  double  lambda;       /* clock rate λ; <= 0 selects -b[1] if b[1] < 0, else 1    */
+  int32_t offspring;    /* rt_offspring                                            */
+  int32_t init_kind;    /* rt_init                                                 */
+  double  init_amp;     /* amp of g                                                */
+  double  init_scale;   /* scale of g (> 0)                                        */
+  int32_t K;            /* orders 0..K are kept; trees with Ne > K are pruned.     */
+                        /* 0 <= K <= 30 and 1 + K*β <= 56 (β = child-digit bits)   */
+  int32_t precision;    /* rt_precision; only RT_PREC_FP64 is implemented          */
+} rt_eq_params;
+
+typedef struct {
+  int64_t trees;        /* trees sampled (kept + pruned)                 */
+  int64_t pruned;       /* trees with Ne > K                             */
+  int64_t particles;    /* particle lifetimes simulated                  */
+  int64_t leaves;       /* g evaluations                                 */
+  int64_t splits;       /* splitting events (incl. the aborting one)     */
+  double  kernel_ms;    /* tree-walk kernel time of the last estimate    */
+  double  total_ms;     /* whole call (host API) or all kernels (_dev)   */
+} rt_stats;
+
+/* A plane x_axis = value carrying an n_per_dim^(d-1) grid over [lo, hi] in
+ * every free axis (PDD artificial interfaces). */
+typedef struct {
+  int32_t axis;
+  double  value;
+  double  lo, hi;
+  int32_t n_per_dim;
+} rt_plane;
+
+/* Per-tree record (debug / parity): structure and contribution of one tree. */
+typedef struct {
+  int32_t ne;          /* splitting events (order bin); > K if pruned   */
+  int32_t leaves;      /* g evaluations                                 */
+  int32_t particles;   /* particles simulated                           */
+  int32_t pruned;      /* 1 if Ne > K                                   */
+  double  C;           /* Π weights × Π g (0 if pruned)                 */
+} rt_tree_rec;
+
+typedef struct rt_handle rt_handle;
+
+/* Validate and normalise the equation (row a1: λ, a_k, support, integer
+ * thresholds, weights) and allocate a handle.
+ * RT_E_ARG on: null pointers, dim ∉ {1,2,3}, D <= 0 or non-finite, degree ∉
+ * [0,8], non-finite b/λ/amp/scale, scale <= 0, K ∉ [0,30], label width
+ * 1 + K*β > 56, a support category of zero integer width, an unknown enum,
+ * precision != RT_PREC_FP64.  An empty support (purely linear f) is legal. */
+rt_status rt_create(const rt_eq_params* params, rt_handle** out);
+
+/* Free the handle and its device scratch.  NULL is a no-op. */
+rt_status rt_destroy(rt_handle* h);
+
+/* Host API (synchronous): copies points to the device, samples n_trees trees
+ * per node, and copies back the per-order coefficients c_n = ΣC_n / N and
+ * standard errors se_n = sqrt(max(0, ΣC_n²/N − c_n²)/(N−1)), n = 0..K, where
+ * N = n_trees counts pruned trees (R4, R11).
+ * RT_E_ARG on: null pointers, n_points < 1, t <= 0 or non-finite, n_trees < 2
+ * or > 2^32, non-finite points.  Times the copies inside rt_stats.total_ms. */
+rt_status rt_estimate(rt_handle* h, const double* points, int64_t n_points, double t,
+                      int64_t n_trees, uint64_t seed,
+                      double* out_coeffs, double* out_stderr);
+
+/* Device API of rt_estimate: d_points [n_points × dim] device, outputs device
+ * [n_points × (K+1)]; stream-ordered on `stream`. */
+rt_status rt_estimate_dev(rt_handle* h, const double* d_points, int64_t n_points, double t,
+                          int64_t n_trees, uint64_t seed,
+                          double* d_out_coeffs, double* d_out_stderr, void* stream);
+
+/* Raw order-binned sums for trees j ∈ [tree_offset, tree_offset + n_trees):
+ * d_sums [n_points × (K+2) × 3] = (ΣC, ΣC², count) per order n = 0..K, and at
+ * n = K+1 the count of pruned trees.  Sums of disjoint tree ranges add, which
+ * is how ranks / calls are merged.  tree_offset + n_trees <= 2^32. */
+rt_status rt_sums_dev(rt_handle* h, const double* d_points, int64_t n_points, double t,
+                      int64_t tree_offset, int64_t n_trees, uint64_t seed,
+                      double* d_sums, void* stream);
+
+/* c_n, se_n (as rt_estimate) and the partial sum u_sum = Σ_n c_n with its
+ * standard error se_sum from d_sums of N_total trees.  Any output may be NULL. */
+rt_status rt_finalize_dev(const double* d_sums, int64_t n_points, int32_t K, int64_t N_total,
+                          double* d_coeffs, double* d_stderr, double* d_u_sum,
+                          double* d_se_sum, void* stream);
+
+/* [L/M] Padé at z = 1 of each node's c_0..c_{L+M} (row stride K+1):
+ * Q(0) = 1, deg P <= L, deg Q <= M, Q Σc_n z^n − P = O(z^{L+M+1}), denominator
+ * by Gaussian elimination with partial pivoting.
+ * out_u [n_points]; out_flags [n_points] (may be NULL): bit0 zero pivot (u =
+ * NaN), bit1 |Q(1)| <= 1e-14 |P(1)|, bit2 Q has a sign change on (0, 1].
+ * RT_E_ARG: null pointers, n_points < 1, L < 0, M < 0, M > 16, L + M > K. */
+rt_status rt_pade(const double* coeffs, int64_t n_points, int32_t K, int32_t L, int32_t M,
+                  double* out_u, uint32_t* out_flags);
+rt_status rt_pade_dev(const double* d_coeffs, int64_t n_points, int32_t K, int32_t L,
+                      int32_t M, double* d_u, uint32_t* d_flags, void* stream);
+
+/* Row a9: place nodes on planes (plane-major; free axes row-major ascending;
+ * linspace(lo, hi, n) = lo + (hi−lo)·(j/(n−1)); exact duplicates of earlier
+ * points skipped; at most max_points kept), then estimate and resum them.
+ * Host buffers: out_points [max_points × dim], out_u, out_stderr (se of the
+ * partial sum, R11), out_flags [max_points]; *out_n_points = count. */
+rt_status rt_interface_values(rt_handle* h, const rt_plane* planes, int32_t n_planes,
+                              int64_t max_points, double t, int64_t n_trees, uint64_t seed,
+                              int32_t L, int32_t M, double* out_points, double* out_u,
+                              double* out_stderr, uint32_t* out_flags,
+                              int64_t* out_n_points);
+
+/* Per-tree records of the production kernel (parity / debugging): for trees
+ * j = tree_offset + s·2^rec_shift (s = 0, 1, …) within [tree_offset,
+ * tree_offset + n_trees) of every node, d_recs[i * n_rec + s] with
+ * n_rec = ceil(n_trees / 2^rec_shift).  The sampled launch is otherwise the
+ * estimate launch; d_sums (may be NULL) receives its sums. */
+rt_status rt_trace_dev(rt_handle* h, const double* d_points, int64_t n_points, double t,
+                       int64_t tree_offset, int64_t n_trees, uint64_t seed, int32_t rec_shift,
+                       rt_tree_rec* d_recs, double* d_sums, void* stream);
+
+/* Counters of the last estimate / sums / trace on this handle. */
+rt_status rt_get_stats(const rt_handle* h, rt_stats* out);
+
+/* Launch geometry override (0 = automatic): CTAs of the tree-walk kernel
+ * and trees per task.  Changes only summation order. */
+rt_status rt_set_launch(rt_handle* h, int32_t grid_ctas, int64_t trees_per_task);
+
+/* The library's Philox4x32-10 block function on device buffers:
+ * d_out[4q..4q+3] = philox(key, d_ctr[4q..4q+3]), q < n (RNG parity tests). */
+rt_status rt_philox_dev(uint64_t key, const uint32_t* d_ctr, int64_t n, uint32_t* d_out,
+                        void* stream);
+
+/* Thread-local message of the last failure on this thread ("" if none). */
+const char* rt_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RT_H */

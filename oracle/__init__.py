@@ -72,6 +72,8 @@ def lib():
                                  C.c_uint64, C.POINTER(TreeRec)]
         _lib.or_trees.argtypes = [C.POINTER(Params), dp, C.c_int64, C.c_double, C.c_int64,
                                   C.c_int64, C.c_uint64, C.c_void_p]
+        _lib.or_trees_at.argtypes = [C.POINTER(Params), dp, C.c_int64, C.c_double, C.c_void_p,
+                                     C.c_int64, C.c_uint64, C.c_void_p]
         _lib.or_sums.argtypes = [C.POINTER(Params), dp, C.c_int64, C.c_double, C.c_int64,
                                  C.c_int64, C.c_uint64, dp, C.POINTER(Stats)]
         _lib.or_finalize.argtypes = [dp, C.c_int64, C.c_int32, C.c_int64, dp, dp, dp, dp]
@@ -129,6 +131,19 @@ def trees(eq: dict, points: np.ndarray, t: float, n_trees: int, seed: int,
                        out.ctypes.data_as(C.c_void_p))
     if e:
         raise ValueError(f"or_trees error {e}")
+    return out
+
+
+def trees_at(eq: dict, points: np.ndarray, t: float, js, seed: int) -> np.ndarray:
+    """Per-tree records [n_points, len(js)] for the tree indices js of every node."""
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    jj = np.ascontiguousarray(np.asarray(js, dtype=np.int64))
+    n = pts.shape[0]
+    out = np.zeros((n, jj.size), dtype=TREE_DTYPE)
+    e = lib().or_trees_at(C.byref(params(eq)), _dp(pts), n, t, jj.ctypes.data_as(C.c_void_p),
+                          jj.size, seed, out.ctypes.data_as(C.c_void_p))
+    if e:
+        raise ValueError(f"or_trees_at error {e}")
     return out
 
 

@@ -223,6 +223,25 @@ int or_trees(const or_params* p, const double* points, int64_t n_points, double 
   return 0;
 }
 
+/* Records for an explicit list of tree indices js[0..n_js) of every node:
+ * rec[i*n_js + q] is tree js[q] of node i (sampled parity at full size). */
+int or_trees_at(const or_params* p, const double* points, int64_t n_points, double t,
+                const int64_t* js, int64_t n_js, uint64_t seed, or_tree_rec* rec) {
+  or_norm nz;
+  int e = or_normalize(p, &nz);
+  if (e) return e;
+  for (int64_t i = 0; i < n_points; ++i)
+    for (int64_t q = 0; q < n_js; ++q) {
+      tree_ctx c = {p, &nz, seed, i, js[q], 0, 0, 0, 0};
+      double C = particle(&c, points + i * p->dim, t, 1u);
+      or_tree_rec* r = rec + i * n_js + q;
+      r->ne = c.ne; r->leaves = c.leaves; r->particles = c.particles;
+      r->pruned = (c.stop == 1);
+      r->C = (c.stop == 1) ? 0.0 : C;
+    }
+  return 0;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Order-binned Monte Carlo sums (Eq. simplecase_discrete:
  * u ≈ (1/N) Σ_j f(β_j); grouping by the number of splitting events,

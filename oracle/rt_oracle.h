@@ -69,6 +69,9 @@ int or_tree(const or_params* p, const double* x, int64_t i, int64_t j, double t,
 int or_trees(const or_params* p, const double* points, int64_t n_points, double t,
              int64_t j0, int64_t n_trees, uint64_t seed, or_tree_rec* rec);
 
+int or_trees_at(const or_params* p, const double* points, int64_t n_points, double t,
+                const int64_t* js, int64_t n_js, uint64_t seed, or_tree_rec* rec);
+
 /* Order-binned sums sums[(i*(K+2)+n)*3 + {0:ΣC, 1:ΣC², 2:count}] for n = 0..K+1
  * (n = K+1 counts pruned trees), over trees j in [j0, j0+n_trees). */
 int or_sums(const or_params* p, const double* points, int64_t n_points, double t,

@@ -1,0 +1,747 @@
+// rt_api.cu — C ABI (include/rt.h) of the B200 random-tree Monte Carlo
+// library: argument validation, equation normalisation (row a1), device
+// scratch management, and the launches of the tree-walk, order-bin
+// reduction, finalisation and batched Padé kernels (rows a3–a9).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <set>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/rt.h"
+#include "philox.cuh"
+#include "tree_walk.cuh"
+
+using rtk::WalkParams;
+
+// ---------------------------------------------------------------------------
+// errors
+static thread_local std::string g_err;
+
+static rt_status fail(rt_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define RT_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(e_ == cudaErrorMemoryAllocation ? RT_E_NOMEM : RT_E_CUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                  \
+  } while (0)
+
+extern "C" const char* rt_last_error(void) { return g_err.c_str(); }
+
+// ---------------------------------------------------------------------------
+// handle
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) cap = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct Norm {
+  double lambda, inv_lambda, sigma;
+  double a[9];
+  int n_support;
+  int support[9];
+  uint64_t thresh[9];
+  double w[9];
+  int beta;
+};
+
+struct rt_handle {
+  rt_eq_params p;
+  Norm nz;
+  cudaStream_t own_stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t last_stream = nullptr;
+  bool have_timing = false;
+  double host_total_ms = -1.0;
+  DevBuf partials, spill, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
+  int32_t grid_override = 0;
+  int64_t tpt_override = 0;
+};
+
+// ---------------------------------------------------------------------------
+// row a1: normalisation.  f(u) = Σ b_k u^k = −λu + Σ a_k u^k with
+// a_k = b_k + λ[k=1]; offspring k with probability p_k and
+// weight a_k/(λ p̂_k); integer thresholds T_k =
+// nearbyint(cum_k · 2^32), last = 2^32, p̂_k = (T_k − T_{k−1})/2^32
+// (R2, R9).  λ default: −b_1 if b_1 < 0 else 1 (R3).
+static rt_status normalize(const rt_eq_params& p, Norm& o) {
+  std::memset(&o, 0, sizeof(o));
+  double lam = p.lambda;
+  if (!(lam > 0.0)) lam = (p.b[1] < 0.0) ? -p.b[1] : 1.0;
+  o.lambda = lam;
+  o.inv_lambda = 1.0 / lam;
+  o.sigma = std::sqrt(2.0 * p.D);
+  int kmax = 0, ns = 0;
+  for (int k = 0; k <= 8; ++k) {
+    double a = (k <= p.degree) ? p.b[k] : 0.0;
+    if (k == 1) a += lam;
+    o.a[k] = a;
+    if (a != 0.0) {
+      o.support[ns++] = k;
+      kmax = k;
+    }
+  }
+  o.n_support = ns;
+  int beta = 1;
+  while ((1 << beta) < kmax) ++beta;
+  o.beta = beta;
+  if (ns == 0) return RT_OK;
+  double prob[9];
+  if (p.offspring == RT_OFFSPRING_UNIFORM) {
+    for (int s = 0; s < ns; ++s) prob[s] = 1.0 / static_cast<double>(ns);
+  } else {
+    double tot = 0.0;
+    for (int s = 0; s < ns; ++s) tot += std::fabs(o.a[o.support[s]]);
+    for (int s = 0; s < ns; ++s) prob[s] = std::fabs(o.a[o.support[s]]) / tot;
+  }
+  const uint64_t two32 = 4294967296ull;
+  double cum = 0.0;
+  uint64_t prev = 0;
+  for (int s = 0; s < ns; ++s) {
+    cum += prob[s];
+    uint64_t T = static_cast<uint64_t>(std::nearbyint(cum * 4294967296.0));
+    if (T > two32 || s == ns - 1) T = two32;
+    if (T <= prev)
+      return fail(RT_E_ARG, "offspring k=%d has zero integer probability width", o.support[s]);
+    o.thresh[s] = T;
+    const double phat = static_cast<double>(T - prev) / 4294967296.0;
+    o.w[s] = o.a[o.support[s]] / (lam * phat);
+    prev = T;
+  }
+  return RT_OK;
+}
+
+static bool is_fin(double v) { return std::isfinite(v); }
+
+extern "C" rt_status rt_create(const rt_eq_params* params, rt_handle** out) {
+  if (!params || !out) return fail(RT_E_ARG, "null pointer");
+  const rt_eq_params& p = *params;
+  if (p.dim < 1 || p.dim > 3) return fail(RT_E_ARG, "dim must be 1, 2 or 3 (got %d)", p.dim);
+  if (!(p.D > 0.0) || !is_fin(p.D)) return fail(RT_E_ARG, "D must be finite and > 0");
+  if (p.degree < 0 || p.degree > 8) return fail(RT_E_ARG, "degree must be in [0, 8]");
+  for (int k = 0; k <= p.degree; ++k)
+    if (!is_fin(p.b[k])) return fail(RT_E_ARG, "b[%d] is not finite", k);
+  if (!is_fin(p.lambda)) return fail(RT_E_ARG, "lambda is not finite");
+  if (p.offspring != RT_OFFSPRING_ABS && p.offspring != RT_OFFSPRING_UNIFORM)
+    return fail(RT_E_ARG, "unknown offspring rule %d", p.offspring);
+  if (p.init_kind < RT_G_CONST || p.init_kind > RT_G_LORENTZ)
+    return fail(RT_E_ARG, "unknown init_kind %d", p.init_kind);
+  if (!is_fin(p.init_amp)) return fail(RT_E_ARG, "init_amp is not finite");
+  if (!(p.init_scale > 0.0) || !is_fin(p.init_scale))
+    return fail(RT_E_ARG, "init_scale must be finite and > 0");
+  if (p.K < 0 || p.K > 30) return fail(RT_E_ARG, "K must be in [0, 30] (got %d)", p.K);
+  if (p.precision != RT_PREC_FP64)
+    return fail(RT_E_ARG, "precision %d is not implemented (only RT_PREC_FP64)", p.precision);
+  Norm nz;
+  rt_status s = normalize(p, nz);
+  if (s != RT_OK) return s;
+  if (1 + p.K * nz.beta > 56)
+    return fail(RT_E_ARG, "label width 1 + K*beta = %d exceeds 56 bits", 1 + p.K * nz.beta);
+  rt_handle* h = new rt_handle();
+  h->p = p;
+  h->nz = nz;
+  cudaError_t e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
+  for (int q = 0; q < 4 && e == cudaSuccess; ++q) e = cudaEventCreate(&h->ev[q]);
+  if (e == cudaSuccess) e = h->stats.ensure(8 * sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    rt_destroy(h);
+    return fail(RT_E_CUDA, "rt_create: %s", cudaGetErrorString(e));
+  }
+  *out = h;
+  return RT_OK;
+}
+
+extern "C" rt_status rt_destroy(rt_handle* h) {
+  if (!h) return RT_OK;
+  if (h->own_stream) cudaStreamSynchronize(h->own_stream);
+  if (h->last_stream) cudaStreamSynchronize(h->last_stream);
+  for (DevBuf* b : {&h->partials, &h->spill, &h->sums, &h->stats, &h->h_points, &h->h_coeffs,
+                    &h->h_stderr, &h->h_aux, &h->h_flags})
+    b->release();
+  for (int q = 0; q < 4; ++q)
+    if (h->ev[q]) cudaEventDestroy(h->ev[q]);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  delete h;
+  return RT_OK;
+}
+
+extern "C" rt_status rt_set_launch(rt_handle* h, int32_t grid_ctas, int64_t trees_per_task) {
+  if (!h) return fail(RT_E_ARG, "null handle");
+  if (grid_ctas < 0 || trees_per_task < 0) return fail(RT_E_ARG, "negative launch override");
+  h->grid_override = grid_ctas;
+  h->tpt_override = trees_per_task;
+  return RT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// tree-walk launch (rows a3–a7)
+template <int DIM>
+struct Lv;
+template <> struct Lv<1> { static constexpr int v = 8; };
+template <> struct Lv<2> { static constexpr int v = 6; };
+template <> struct Lv<3> { static constexpr int v = 5; };
+
+using KernelFn = void (*)(WalkParams);
+
+template <int DIM, int GK, bool REC>
+static KernelFn pick_kernel() {
+  return rtk::tree_walk_kernel<DIM, GK, Lv<DIM>::v, REC>;
+}
+
+static KernelFn kernel_for(int dim, int gk, bool rec, int* lv, int* smem) {
+#define RT_K(D, G)                                                              \
+  if (dim == D && gk == G) {                                                    \
+    *lv = Lv<D>::v;                                                             \
+    *smem = rtk::smem_bytes<D, Lv<D>::v>();                                     \
+    return rec ? pick_kernel<D, G, true>() : pick_kernel<D, G, false>();        \
+  }
+  RT_K(1, 0) RT_K(1, 1) RT_K(1, 2) RT_K(1, 3)
+  RT_K(2, 0) RT_K(2, 1) RT_K(2, 2) RT_K(2, 3)
+  RT_K(3, 0) RT_K(3, 1) RT_K(3, 2) RT_K(3, 3)
+#undef RT_K
+  return nullptr;
+}
+
+struct Launch {
+  int grid;
+  int64_t T, tpn, n_tasks;
+};
+
+static rt_status plan_launch(rt_handle* h, KernelFn fn, int smem, int64_t n_points,
+                             int64_t n_trees, Launch& L) {
+  int dev = 0, nsm = 0, per_sm = 0;
+  RT_CUDA(cudaGetDevice(&dev));
+  RT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  RT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, rtk::kThreads,
+                                                        smem));
+  if (per_sm < 1) return fail(RT_E_CUDA, "tree_walk kernel cannot be resident");
+  int grid = nsm * per_sm;
+  if (h->grid_override > 0) grid = h->grid_override;
+  const int64_t warps = static_cast<int64_t>(grid) * rtk::kWarpsPerCta;
+  const int64_t total = n_points * n_trees;
+  int64_t T = h->tpt_override;
+  if (T <= 0) {
+    // >= ~32 tasks per warp keeps the static round-robin balanced to ~3 %
+    T = total / (warps * 32);
+    T = std::max<int64_t>(T, 512);
+    T = std::min<int64_t>(T, 65536);
+  }
+  T = std::min<int64_t>(T, n_trees);
+  L.T = T;
+  L.tpn = (n_trees + T - 1) / T;
+  L.n_tasks = n_points * L.tpn;
+  const int64_t need_ctas = (L.n_tasks + rtk::kWarpsPerCta - 1) / rtk::kWarpsPerCta;
+  L.grid = static_cast<int>(std::min<int64_t>(grid, need_ctas));
+  return RT_OK;
+}
+
+__global__ void reduce_tasks_kernel(const double* __restrict__ partials, int64_t tpn, int nb,
+                                    double* __restrict__ sums) {
+  // second pass: node i's tasks summed in task order (atomic-free, deterministic)
+  const int64_t i = blockIdx.x;
+  const int b = threadIdx.x;
+  if (b >= nb) return;
+  double s1 = 0.0, s2 = 0.0, c = 0.0;
+  const double* p = partials + (i * tpn * nb + b) * 3;
+  for (int64_t q = 0; q < tpn; ++q, p += static_cast<int64_t>(nb) * 3) {
+    s1 += p[0];
+    s2 += p[1];
+    c += p[2];
+  }
+  double* o = sums + (i * nb + b) * 3;
+  o[0] = s1;
+  o[1] = s2;
+  o[2] = c;
+}
+
+__global__ void finalize_kernel(const double* __restrict__ sums, int K, double N,
+                                double* __restrict__ coeffs, double* __restrict__ se,
+                                double* __restrict__ u_sum, double* __restrict__ se_sum) {
+  // c_n = ΣC_n/N, se_n = sqrt(max(0, ΣC_n²/N − c_n²)/(N−1)) (R4, R11)
+  const int64_t i = blockIdx.x;
+  const int b = threadIdx.x;
+  const int nb = K + 2;
+  double c = 0.0, s2 = 0.0;
+  if (b <= K) {
+    const double* s = sums + (i * nb + b) * 3;
+    c = s[0] / N;
+    s2 = s[1];
+    const double v = s2 / N - c * c;
+    if (coeffs) coeffs[i * (K + 1) + b] = c;
+    if (se) se[i * (K + 1) + b] = sqrt((v > 0.0 ? v : 0.0) / (N - 1.0));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if (b == 0) {
+    if (u_sum) u_sum[i] = c;
+    if (se_sum) {
+      const double v = s2 / N - c * c;
+      se_sum[i] = sqrt((v > 0.0 ? v : 0.0) / (N - 1.0));
+    }
+  }
+}
+
+static rt_status check_run_args(const rt_handle* h, int64_t n_points, double t,
+                                int64_t tree_offset, int64_t n_trees) {
+  if (!h) return fail(RT_E_ARG, "null handle");
+  if (n_points < 1) return fail(RT_E_ARG, "n_points must be >= 1");
+  if (!(t > 0.0) || !is_fin(t)) return fail(RT_E_ARG, "t must be finite and > 0");
+  if (n_trees < 2) return fail(RT_E_ARG, "n_trees must be >= 2");
+  if (tree_offset < 0 || tree_offset + n_trees > (int64_t(1) << 32))
+    return fail(RT_E_ARG, "tree range must lie in [0, 2^32)");
+  if (n_points > (int64_t(1) << 31)) return fail(RT_E_ARG, "n_points too large");
+  return RT_OK;
+}
+
+// Runs the tree walk + task reduction; d_sums receives [n][K+2][3].
+static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points, double t,
+                          int64_t tree_offset, int64_t n_trees, uint64_t seed, int rec_shift,
+                          rtk::TreeRec* d_recs, double* d_sums, cudaStream_t st) {
+  const rt_eq_params& p = h->p;
+  const Norm& nz = h->nz;
+  int lv = 0, smem = 0;
+  KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, &lv, &smem);
+  if (!fn) return fail(RT_E_ARG, "no kernel for dim=%d init_kind=%d", p.dim, p.init_kind);
+  Launch L;
+  rt_status s = plan_launch(h, fn, smem, n_points, n_trees, L);
+  if (s != RT_OK) return s;
+  const int nb = p.K + 2;
+  const int nf = p.dim + 2;
+  const int spill_levels = std::max(0, p.K - lv);
+  RT_CUDA(h->partials.ensure(static_cast<size_t>(L.n_tasks) * nb * 3 * sizeof(double)));
+  const size_t spill_bytes = static_cast<size_t>(L.grid) * rtk::kWarpsPerCta * spill_levels *
+                             nf * 32 * sizeof(double);
+  RT_CUDA(h->spill.ensure(std::max<size_t>(spill_bytes, 256)));
+
+  WalkParams P;
+  std::memset(&P, 0, sizeof(P));
+  P.rk = rtk::make_round_keys(seed);
+  P.inv_lambda = nz.inv_lambda;
+  P.sigma = nz.sigma;
+  P.amp = p.init_amp;
+  P.inv_scale = 1.0 / p.init_scale;
+  P.inv_scale2 = 1.0 / (p.init_scale * p.init_scale);
+  P.t = t;
+  for (int q = 0; q < nz.n_support; ++q) {
+    P.w[q] = nz.w[q];
+    P.thr[q] = static_cast<uint32_t>(nz.thresh[q] - 1);
+    P.kval[q] = nz.support[q];
+  }
+  P.n_support = nz.n_support;
+  P.beta = nz.beta;
+  P.K = p.K;
+  P.nb = nb;
+  P.points = d_points;
+  P.n_trees = n_trees;
+  P.tree_offset = tree_offset;
+  P.T = L.T;
+  P.tpn = L.tpn;
+  P.n_tasks = L.n_tasks;
+  P.partials = static_cast<double*>(h->partials.p);
+  P.spill = static_cast<double*>(h->spill.p);
+  P.spill_levels = spill_levels;
+  P.recs = d_recs;
+  P.rec_shift = rec_shift;
+  P.n_rec = (n_trees + (int64_t(1) << rec_shift) - 1) >> rec_shift;
+  P.stats = static_cast<unsigned long long*>(h->stats.p);
+
+  RT_CUDA(cudaMemsetAsync(h->stats.p, 0, 5 * sizeof(unsigned long long), st));
+  RT_CUDA(cudaEventRecord(h->ev[0], st));
+  fn<<<L.grid, rtk::kThreads, smem, st>>>(P);
+  RT_CUDA(cudaGetLastError());
+  RT_CUDA(cudaEventRecord(h->ev[1], st));
+  reduce_tasks_kernel<<<static_cast<unsigned>(n_points), 32, 0, st>>>(
+      static_cast<double*>(h->partials.p), L.tpn, nb, d_sums);
+  RT_CUDA(cudaGetLastError());
+  h->last_stream = st;
+  h->have_timing = true;
+  h->host_total_ms = -1.0;
+  return RT_OK;
+}
+
+extern "C" rt_status rt_sums_dev(rt_handle* h, const double* d_points, int64_t n_points,
+                                 double t, int64_t tree_offset, int64_t n_trees, uint64_t seed,
+                                 double* d_sums, void* stream) {
+  rt_status s = check_run_args(h, n_points, t, tree_offset, n_trees);
+  if (s != RT_OK) return s;
+  if (!d_points || !d_sums) return fail(RT_E_ARG, "null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  s = run_walk(h, d_points, n_points, t, tree_offset, n_trees, seed, 0, nullptr, d_sums, st);
+  if (s != RT_OK) return s;
+  RT_CUDA(cudaEventRecord(h->ev[2], st));
+  return RT_OK;
+}
+
+extern "C" rt_status rt_finalize_dev(const double* d_sums, int64_t n_points, int32_t K,
+                                     int64_t N_total, double* d_coeffs, double* d_stderr,
+                                     double* d_u_sum, double* d_se_sum, void* stream) {
+  if (!d_sums) return fail(RT_E_ARG, "null sums");
+  if (n_points < 1 || K < 0 || K > 30 || N_total < 2) return fail(RT_E_ARG, "bad sizes");
+  finalize_kernel<<<static_cast<unsigned>(n_points), 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_sums, K, static_cast<double>(N_total), d_coeffs, d_stderr, d_u_sum, d_se_sum);
+  RT_CUDA(cudaGetLastError());
+  return RT_OK;
+}
+
+extern "C" rt_status rt_estimate_dev(rt_handle* h, const double* d_points, int64_t n_points,
+                                     double t, int64_t n_trees, uint64_t seed,
+                                     double* d_out_coeffs, double* d_out_stderr, void* stream) {
+  rt_status s = check_run_args(h, n_points, t, 0, n_trees);
+  if (s != RT_OK) return s;
+  if (!d_points || !d_out_coeffs || !d_out_stderr) return fail(RT_E_ARG, "null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nb = h->p.K + 2;
+  RT_CUDA(h->sums.ensure(static_cast<size_t>(n_points) * nb * 3 * sizeof(double)));
+  double* sums = static_cast<double*>(h->sums.p);
+  s = run_walk(h, d_points, n_points, t, 0, n_trees, seed, 0, nullptr, sums, st);
+  if (s != RT_OK) return s;
+  finalize_kernel<<<static_cast<unsigned>(n_points), 32, 0, st>>>(
+      sums, h->p.K, static_cast<double>(n_trees), d_out_coeffs, d_out_stderr, nullptr, nullptr);
+  RT_CUDA(cudaGetLastError());
+  RT_CUDA(cudaEventRecord(h->ev[2], st));
+  return RT_OK;
+}
+
+extern "C" rt_status rt_trace_dev(rt_handle* h, const double* d_points, int64_t n_points,
+                                  double t, int64_t tree_offset, int64_t n_trees, uint64_t seed,
+                                  int32_t rec_shift, rt_tree_rec* d_recs, double* d_sums,
+                                  void* stream) {
+  rt_status s = check_run_args(h, n_points, t, tree_offset, n_trees);
+  if (s != RT_OK) return s;
+  if (!d_points || !d_recs) return fail(RT_E_ARG, "null pointer");
+  if (rec_shift < 0 || rec_shift > 31) return fail(RT_E_ARG, "rec_shift must be in [0, 31]");
+  static_assert(sizeof(rt_tree_rec) == sizeof(rtk::TreeRec), "record layout");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nb = h->p.K + 2;
+  double* sums = d_sums;
+  if (!sums) {
+    RT_CUDA(h->sums.ensure(static_cast<size_t>(n_points) * nb * 3 * sizeof(double)));
+    sums = static_cast<double*>(h->sums.p);
+  }
+  s = run_walk(h, d_points, n_points, t, tree_offset, n_trees, seed, rec_shift,
+               reinterpret_cast<rtk::TreeRec*>(d_recs), sums, st);
+  if (s != RT_OK) return s;
+  RT_CUDA(cudaEventRecord(h->ev[2], st));
+  return RT_OK;
+}
+
+extern "C" rt_status rt_get_stats(const rt_handle* hc, rt_stats* out) {
+  if (!hc || !out) return fail(RT_E_ARG, "null pointer");
+  rt_handle* h = const_cast<rt_handle*>(hc);
+  std::memset(out, 0, sizeof(*out));
+  if (!h->have_timing) return RT_OK;
+  RT_CUDA(cudaEventSynchronize(h->ev[2]));
+  unsigned long long v[5];
+  RT_CUDA(cudaMemcpy(v, h->stats.p, sizeof(v), cudaMemcpyDeviceToHost));
+  out->trees = static_cast<int64_t>(v[0]);
+  out->pruned = static_cast<int64_t>(v[1]);
+  out->particles = static_cast<int64_t>(v[2]);
+  out->leaves = static_cast<int64_t>(v[3]);
+  out->splits = static_cast<int64_t>(v[4]);
+  float ms = 0.f;
+  RT_CUDA(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+  out->kernel_ms = ms;
+  if (h->host_total_ms >= 0.0) {
+    out->total_ms = h->host_total_ms;
+  } else {
+    RT_CUDA(cudaEventElapsedTime(&ms, h->ev[0], h->ev[2]));
+    out->total_ms = ms;
+  }
+  return RT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host API
+static rt_status check_points_host(const double* pts, int64_t n, int dim) {
+  for (int64_t q = 0; q < n * dim; ++q)
+    if (!is_fin(pts[q])) return fail(RT_E_ARG, "point coordinate %lld is not finite", (long long)q);
+  return RT_OK;
+}
+
+extern "C" rt_status rt_estimate(rt_handle* h, const double* points, int64_t n_points, double t,
+                                 int64_t n_trees, uint64_t seed, double* out_coeffs,
+                                 double* out_stderr) {
+  rt_status s = check_run_args(h, n_points, t, 0, n_trees);
+  if (s != RT_OK) return s;
+  if (!points || !out_coeffs || !out_stderr) return fail(RT_E_ARG, "null pointer");
+  s = check_points_host(points, n_points, h->p.dim);
+  if (s != RT_OK) return s;
+  cudaStream_t st = h->own_stream;
+  const size_t pb = static_cast<size_t>(n_points) * h->p.dim * sizeof(double);
+  const size_t cb = static_cast<size_t>(n_points) * (h->p.K + 1) * sizeof(double);
+  RT_CUDA(h->h_points.ensure(pb));
+  RT_CUDA(h->h_coeffs.ensure(cb));
+  RT_CUDA(h->h_stderr.ensure(cb));
+  RT_CUDA(cudaEventRecord(h->ev[3], st));
+  RT_CUDA(cudaMemcpyAsync(h->h_points.p, points, pb, cudaMemcpyHostToDevice, st));
+  s = rt_estimate_dev(h, static_cast<double*>(h->h_points.p), n_points, t, n_trees, seed,
+                      static_cast<double*>(h->h_coeffs.p), static_cast<double*>(h->h_stderr.p),
+                      st);
+  if (s != RT_OK) return s;
+  RT_CUDA(cudaMemcpyAsync(out_coeffs, h->h_coeffs.p, cb, cudaMemcpyDeviceToHost, st));
+  RT_CUDA(cudaMemcpyAsync(out_stderr, h->h_stderr.p, cb, cudaMemcpyDeviceToHost, st));
+  RT_CUDA(cudaEventRecord(h->ev[2], st));
+  RT_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  RT_CUDA(cudaEventElapsedTime(&ms, h->ev[3], h->ev[2]));
+  h->host_total_ms = ms;
+  return RT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// row a8: batched [L/M] Padé, one thread per node (negligible cost, M <= 16)
+__global__ void pade_kernel(const double* __restrict__ coeffs, int64_t n, int stride, int L,
+                            int M, double* __restrict__ out_u, uint32_t* __restrict__ flags) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* c = coeffs + i * stride;
+  double A[16][17];
+  double q[17];
+  uint32_t fl = 0;
+  // Toeplitz system Σ_j q_j c_{L+r-j} = -c_{L+r}, r = 1..M
+  for (int r = 0; r < M; ++r) {
+    for (int j = 0; j < M; ++j) {
+      const int idx = L + r - j;
+      A[r][j] = idx >= 0 ? c[idx] : 0.0;
+    }
+    A[r][M] = -c[L + r + 1];
+  }
+  for (int col = 0; col < M && !(fl & 1u); ++col) {
+    int piv = col;
+    double best = fabs(A[col][col]);
+    for (int r = col + 1; r < M; ++r) {
+      const double v = fabs(A[r][col]);
+      if (v > best) { best = v; piv = r; }
+    }
+    if (best == 0.0) { fl |= 1u; break; }
+    if (piv != col)
+      for (int k = col; k <= M; ++k) { const double tmp = A[col][k]; A[col][k] = A[piv][k]; A[piv][k] = tmp; }
+    for (int r = col + 1; r < M; ++r) {
+      const double f = A[r][col] / A[col][col];
+      for (int k = col; k <= M; ++k) A[r][k] = __dsub_rn(A[r][k], __dmul_rn(f, A[col][k]));
+    }
+  }
+  if (fl & 1u) {
+    out_u[i] = __longlong_as_double(0x7ff8000000000000ll);
+    if (flags) flags[i] = fl;
+    return;
+  }
+  q[0] = 1.0;
+  for (int r = M - 1; r >= 0; --r) {
+    double s = A[r][M];
+    for (int k = r + 1; k < M; ++k) s = __dsub_rn(s, __dmul_rn(A[r][k], q[k + 1]));
+    q[r + 1] = s / A[r][r];
+  }
+  double P1 = 0.0, Q1 = 0.0;
+  for (int a = 0; a <= L; ++a) {
+    double pa = 0.0;
+    const int jm = a < M ? a : M;
+    for (int j = 0; j <= jm; ++j) pa = __dadd_rn(pa, __dmul_rn(q[j], c[a - j]));
+    P1 += pa;
+  }
+  for (int j = 0; j <= M; ++j) Q1 += q[j];
+  out_u[i] = P1 / Q1;
+  if (fabs(Q1) <= 1e-14 * fabs(P1)) fl |= 2u;
+  for (int s = 1; s <= 256; ++s) {
+    const double z = static_cast<double>(s) / 256.0;
+    double Qz = 0.0, zp = 1.0;
+    for (int j = 0; j <= M; ++j) { Qz = __dadd_rn(Qz, __dmul_rn(q[j], zp)); zp *= z; }
+    if (!(Qz > 0.0)) { fl |= 4u; break; }
+  }
+  if (flags) flags[i] = fl;
+}
+
+static rt_status check_pade_args(int64_t n_points, int32_t K, int32_t L, int32_t M) {
+  if (n_points < 1) return fail(RT_E_ARG, "n_points must be >= 1");
+  if (L < 0 || M < 0 || M > 16 || L + M > K)
+    return fail(RT_E_ARG, "need 0 <= L, 0 <= M <= 16, L + M <= K (L=%d M=%d K=%d)", L, M, K);
+  return RT_OK;
+}
+
+extern "C" rt_status rt_pade_dev(const double* d_coeffs, int64_t n_points, int32_t K, int32_t L,
+                                 int32_t M, double* d_u, uint32_t* d_flags, void* stream) {
+  if (!d_coeffs || !d_u) return fail(RT_E_ARG, "null pointer");
+  rt_status s = check_pade_args(n_points, K, L, M);
+  if (s != RT_OK) return s;
+  const unsigned blocks = static_cast<unsigned>((n_points + 127) / 128);
+  pade_kernel<<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(d_coeffs, n_points, K + 1,
+                                                                      L, M, d_u, d_flags);
+  RT_CUDA(cudaGetLastError());
+  return RT_OK;
+}
+
+extern "C" rt_status rt_pade(const double* coeffs, int64_t n_points, int32_t K, int32_t L,
+                             int32_t M, double* out_u, uint32_t* out_flags) {
+  if (!coeffs || !out_u) return fail(RT_E_ARG, "null pointer");
+  rt_status s = check_pade_args(n_points, K, L, M);
+  if (s != RT_OK) return s;
+  const size_t cb = static_cast<size_t>(n_points) * (K + 1) * sizeof(double);
+  double *dc = nullptr, *du = nullptr;
+  uint32_t* df = nullptr;
+  RT_CUDA(cudaMalloc(&dc, cb));
+  cudaError_t e = cudaMalloc(&du, n_points * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&df, n_points * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemcpy(dc, coeffs, cb, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    pade_kernel<<<static_cast<unsigned>((n_points + 127) / 128), 128>>>(dc, n_points, K + 1, L, M,
+                                                                         du, df);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out_u, du, n_points * sizeof(double), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && out_flags)
+    e = cudaMemcpy(out_flags, df, n_points * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+  cudaFree(dc);
+  cudaFree(du);
+  cudaFree(df);
+  if (e != cudaSuccess) return fail(RT_E_CUDA, "rt_pade: %s", cudaGetErrorString(e));
+  return RT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// row a9: interface nodes on planes (R14)
+static double lin(double lo, double hi, int n, int j) {
+  if (n == 1) return lo;
+  return lo + (hi - lo) * (static_cast<double>(j) / static_cast<double>(n - 1));
+}
+
+static rt_status place_nodes(int dim, const rt_plane* planes, int32_t n_planes,
+                             int64_t max_points, std::vector<double>& pts) {
+  std::set<std::vector<double>> seen;
+  pts.clear();
+  int64_t count = 0;
+  for (int32_t pl = 0; pl < n_planes && count < max_points; ++pl) {
+    const rt_plane& P = planes[pl];
+    if (P.axis < 0 || P.axis >= dim) return fail(RT_E_ARG, "plane %d: axis out of range", pl);
+    if (P.n_per_dim < 1) return fail(RT_E_ARG, "plane %d: n_per_dim must be >= 1", pl);
+    if (!is_fin(P.value) || !is_fin(P.lo) || !is_fin(P.hi))
+      return fail(RT_E_ARG, "plane %d: non-finite bounds", pl);
+    int free_ax[2] = {0, 0}, nfree = 0;
+    for (int a = 0; a < dim; ++a)
+      if (a != P.axis) free_ax[nfree++] = a;
+    int64_t total = 1;
+    for (int f = 0; f < nfree; ++f) total *= P.n_per_dim;
+    for (int64_t idx = 0; idx < total && count < max_points; ++idx) {
+      std::vector<double> x(dim, 0.0);
+      x[P.axis] = P.value;
+      int64_t rem = idx;
+      for (int f = nfree - 1; f >= 0; --f) {   // row-major: last free axis fastest
+        const int j = static_cast<int>(rem % P.n_per_dim);
+        rem /= P.n_per_dim;
+        x[free_ax[f]] = lin(P.lo, P.hi, P.n_per_dim, j);
+      }
+      if (!seen.insert(x).second) continue;
+      pts.insert(pts.end(), x.begin(), x.end());
+      ++count;
+    }
+  }
+  return RT_OK;
+}
+
+extern "C" rt_status rt_interface_values(rt_handle* h, const rt_plane* planes, int32_t n_planes,
+                                         int64_t max_points, double t, int64_t n_trees,
+                                         uint64_t seed, int32_t L, int32_t M, double* out_points,
+                                         double* out_u, double* out_stderr, uint32_t* out_flags,
+                                         int64_t* out_n_points) {
+  if (!h || !planes || !out_points || !out_u || !out_stderr || !out_n_points)
+    return fail(RT_E_ARG, "null pointer");
+  if (n_planes < 1 || max_points < 1) return fail(RT_E_ARG, "need n_planes >= 1, max_points >= 1");
+  const int K = h->p.K;
+  rt_status s = check_pade_args(1, K, L, M);
+  if (s != RT_OK) return s;
+  std::vector<double> pts;
+  s = place_nodes(h->p.dim, planes, n_planes, max_points, pts);
+  if (s != RT_OK) return s;
+  const int64_t n = static_cast<int64_t>(pts.size()) / h->p.dim;
+  if (n < 1) return fail(RT_E_ARG, "no nodes placed");
+  s = check_run_args(h, n, t, 0, n_trees);
+  if (s != RT_OK) return s;
+  cudaStream_t st = h->own_stream;
+  const int nb = K + 2;
+  RT_CUDA(h->h_points.ensure(pts.size() * sizeof(double)));
+  RT_CUDA(h->h_coeffs.ensure(static_cast<size_t>(n) * (K + 1) * sizeof(double)));
+  RT_CUDA(h->h_stderr.ensure(static_cast<size_t>(n) * 2 * sizeof(double)));
+  RT_CUDA(h->h_flags.ensure(static_cast<size_t>(n) * sizeof(uint32_t)));
+  RT_CUDA(h->sums.ensure(static_cast<size_t>(n) * nb * 3 * sizeof(double)));
+  double* d_pts = static_cast<double*>(h->h_points.p);
+  double* d_c = static_cast<double*>(h->h_coeffs.p);
+  double* d_u = static_cast<double*>(h->h_stderr.p);
+  double* d_se = d_u + n;
+  uint32_t* d_fl = static_cast<uint32_t*>(h->h_flags.p);
+  double* d_sums = static_cast<double*>(h->sums.p);
+  RT_CUDA(cudaEventRecord(h->ev[3], st));
+  RT_CUDA(cudaMemcpyAsync(d_pts, pts.data(), pts.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  s = run_walk(h, d_pts, n, t, 0, n_trees, seed, 0, nullptr, d_sums, st);
+  if (s != RT_OK) return s;
+  finalize_kernel<<<static_cast<unsigned>(n), 32, 0, st>>>(d_sums, K, static_cast<double>(n_trees),
+                                                            d_c, nullptr, nullptr, d_se);
+  RT_CUDA(cudaGetLastError());
+  pade_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(d_c, n, K + 1, L, M, d_u, d_fl);
+  RT_CUDA(cudaGetLastError());
+  RT_CUDA(cudaEventRecord(h->ev[2], st));
+  RT_CUDA(cudaMemcpyAsync(out_points, d_pts, pts.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  RT_CUDA(cudaMemcpyAsync(out_u, d_u, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  RT_CUDA(cudaMemcpyAsync(out_stderr, d_se, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (out_flags)
+    RT_CUDA(cudaMemcpyAsync(out_flags, d_fl, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  RT_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  RT_CUDA(cudaEventElapsedTime(&ms, h->ev[3], h->ev[2]));
+  h->host_total_ms = ms;
+  *out_n_points = n;
+  return RT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// RNG parity hook
+__global__ void philox_kernel(rtk::RoundKeys rk, const uint32_t* __restrict__ ctr, int64_t n,
+                              uint32_t* __restrict__ out) {
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const uint4 r = rtk::philox4x32_10(ctr[4 * q], ctr[4 * q + 1], ctr[4 * q + 2], ctr[4 * q + 3], rk);
+  out[4 * q] = r.x;
+  out[4 * q + 1] = r.y;
+  out[4 * q + 2] = r.z;
+  out[4 * q + 3] = r.w;
+}
+
+extern "C" rt_status rt_philox_dev(uint64_t key, const uint32_t* d_ctr, int64_t n, uint32_t* d_out,
+                                   void* stream) {
+  if (!d_ctr || !d_out) return fail(RT_E_ARG, "null pointer");
+  if (n < 1) return fail(RT_E_ARG, "n must be >= 1");
+  philox_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      rtk::make_round_keys(key), d_ctr, n, d_out);
+  RT_CUDA(cudaGetLastError());
+  return RT_OK;
+}
