@@ -205,24 +205,21 @@ extern "C" rt_status rt_set_launch(rt_handle* h, int32_t grid_ctas, int64_t tree
 
 // ---------------------------------------------------------------------------
 // tree-walk launch (rows a3–a7)
-template <int DIM>
-struct Lv;
-template <> struct Lv<1> { static constexpr int v = 8; };
-template <> struct Lv<2> { static constexpr int v = 6; };
-template <> struct Lv<3> { static constexpr int v = 5; };
-
 using KernelFn = void (*)(WalkParams);
 
 template <int DIM, int GK, bool REC>
 static KernelFn pick_kernel() {
-  return rtk::tree_walk_kernel<DIM, GK, Lv<DIM>::v, REC>;
+  return rtk::tree_walk_kernel<DIM, GK, REC>;
 }
 
-static KernelFn kernel_for(int dim, int gk, bool rec, int* lv, int* smem) {
+// The kernel for (dim, g, rec) and the production (rec = false) kernel whose
+// occupancy fixes the launch geometry for both.
+static KernelFn kernel_for(int dim, int gk, bool rec, KernelFn* prod, int* smem, int* levels) {
 #define RT_K(D, G)                                                              \
   if (dim == D && gk == G) {                                                    \
-    *lv = Lv<D>::v;                                                             \
-    *smem = rtk::smem_bytes<D, Lv<D>::v>();                                     \
+    *smem = rtk::smem_bytes<D>();                                               \
+    *levels = rtk::Levels<D>::v;                                                \
+    *prod = pick_kernel<D, G, false>();                                         \
     return rec ? pick_kernel<D, G, true>() : pick_kernel<D, G, false>();        \
   }
   RT_K(1, 0) RT_K(1, 1) RT_K(1, 2) RT_K(1, 3)
@@ -257,6 +254,9 @@ static rt_status plan_launch(rt_handle* h, KernelFn fn, int smem, int64_t n_poin
     T = std::min<int64_t>(T, 65536);
   }
   T = std::min<int64_t>(T, n_trees);
+  // task ids are 32-bit in the kernel: grow tasks until they number < 2^31
+  while (n_points * ((n_trees + T - 1) / T) >= (int64_t(1) << 31)) T *= 2;
+  T = std::min<int64_t>(T, n_trees);
   L.T = T;
   L.tpn = (n_trees + T - 1) / T;
   L.n_tasks = n_points * L.tpn;
@@ -266,22 +266,37 @@ static rt_status plan_launch(rt_handle* h, KernelFn fn, int smem, int64_t n_poin
 }
 
 __global__ void reduce_tasks_kernel(const double* __restrict__ partials, int64_t tpn, int nb,
-                                    double* __restrict__ sums) {
-  // second pass: node i's tasks summed in task order (atomic-free, deterministic)
+                                    double* __restrict__ sums,
+                                    unsigned long long* __restrict__ stats) {
+  // second pass: node i's tasks summed in task order (atomic-free, deterministic);
+  // the exact bin counts also give trees, pruned trees and splits (a pruned
+  // tree aborted at its (K+1)-th split)
   const int64_t i = blockIdx.x;
   const int b = threadIdx.x;
-  if (b >= nb) return;
   double s1 = 0.0, s2 = 0.0, c = 0.0;
-  const double* p = partials + (i * tpn * nb + b) * 3;
-  for (int64_t q = 0; q < tpn; ++q, p += static_cast<int64_t>(nb) * 3) {
-    s1 += p[0];
-    s2 += p[1];
-    c += p[2];
+  if (b < nb) {
+    const double* p = partials + (i * tpn * nb + b) * 3;
+    for (int64_t q = 0; q < tpn; ++q, p += static_cast<int64_t>(nb) * 3) {
+      s1 += p[0];
+      s2 += p[1];
+      c += p[2];
+    }
+    double* o = sums + (i * nb + b) * 3;
+    o[0] = s1;
+    o[1] = s2;
+    o[2] = c;
   }
-  double* o = sums + (i * nb + b) * 3;
-  o[0] = s1;
-  o[1] = s2;
-  o[2] = c;
+  unsigned long long trees = static_cast<unsigned long long>(c);
+  unsigned long long splits = trees * static_cast<unsigned long long>(b);
+  for (int o = 16; o > 0; o >>= 1) {
+    trees += __shfl_xor_sync(0xffffffffu, trees, o);
+    splits += __shfl_xor_sync(0xffffffffu, splits, o);
+  }
+  if (b == 0) {
+    atomicAdd(stats + 0, trees);
+    atomicAdd(stats + 4, splits);
+  }
+  if (b == nb - 1) atomicAdd(stats + 1, static_cast<unsigned long long>(c));
 }
 
 __global__ void finalize_kernel(const double* __restrict__ sums, int K, double N,
@@ -321,6 +336,7 @@ static rt_status check_run_args(const rt_handle* h, int64_t n_points, double t,
   if (n_trees < 2) return fail(RT_E_ARG, "n_trees must be >= 2");
   if (tree_offset < 0 || tree_offset + n_trees > (int64_t(1) << 32))
     return fail(RT_E_ARG, "tree range must lie in [0, 2^32)");
+  if (n_trees >= (int64_t(1) << 31)) return fail(RT_E_ARG, "n_trees must be < 2^31 per call");
   if (n_points > (int64_t(1) << 31)) return fail(RT_E_ARG, "n_points too large");
   return RT_OK;
 }
@@ -331,16 +347,22 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
                           rtk::TreeRec* d_recs, double* d_sums, cudaStream_t st) {
   const rt_eq_params& p = h->p;
   const Norm& nz = h->nz;
-  int lv = 0, smem = 0;
-  KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, &lv, &smem);
+  int smem = 0, levels = 0;
+  KernelFn prod = nullptr;
+  KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, &prod, &smem, &levels);
   if (!fn) return fail(RT_E_ARG, "no kernel for dim=%d init_kind=%d", p.dim, p.init_kind);
+  if (smem > 48 * 1024) {
+    RT_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    RT_CUDA(cudaFuncSetAttribute((const void*)prod, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  }
   Launch L;
-  rt_status s = plan_launch(h, fn, smem, n_points, n_trees, L);
+  rt_status s = plan_launch(h, prod, smem, n_points, n_trees, L);   // same grid for the trace
   if (s != RT_OK) return s;
   const int nb = p.K + 2;
   const int nf = p.dim + 2;
-  const int spill_levels = std::max(0, p.K - lv);
   RT_CUDA(h->partials.ensure(static_cast<size_t>(L.n_tasks) * nb * 3 * sizeof(double)));
+  // stack levels beyond the shared-memory ones: [warps][K - LV][nf][32] doubles
+  const int spill_levels = std::max(0, p.K - levels);
   const size_t spill_bytes = static_cast<size_t>(L.grid) * rtk::kWarpsPerCta * spill_levels *
                              nf * 32 * sizeof(double);
   RT_CUDA(h->spill.ensure(std::max<size_t>(spill_bytes, 256)));
@@ -349,11 +371,12 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   std::memset(&P, 0, sizeof(P));
   P.rk = rtk::make_round_keys(seed);
   P.inv_lambda = nz.inv_lambda;
-  P.sigma = nz.sigma;
+  P.two_d = 2.0 * p.D;
   P.amp = p.init_amp;
   P.inv_scale = 1.0 / p.init_scale;
   P.inv_scale2 = 1.0 / (p.init_scale * p.init_scale);
   P.t = t;
+  for (int q = 0; q < 9; ++q) P.thr[q] = 0xffffffffu;
   for (int q = 0; q < nz.n_support; ++q) {
     P.w[q] = nz.w[q];
     P.thr[q] = static_cast<uint32_t>(nz.thresh[q] - 1);
@@ -364,11 +387,11 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   P.K = p.K;
   P.nb = nb;
   P.points = d_points;
-  P.n_trees = n_trees;
-  P.tree_offset = tree_offset;
-  P.T = L.T;
-  P.tpn = L.tpn;
-  P.n_tasks = L.n_tasks;
+  P.n_trees = static_cast<int32_t>(n_trees);
+  P.tree_offset = static_cast<uint32_t>(tree_offset);
+  P.T = static_cast<int32_t>(L.T);
+  P.tpn = static_cast<int32_t>(L.tpn);
+  P.n_tasks = static_cast<int32_t>(L.n_tasks);
   P.partials = static_cast<double*>(h->partials.p);
   P.spill = static_cast<double*>(h->spill.p);
   P.spill_levels = spill_levels;
@@ -383,7 +406,8 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   RT_CUDA(cudaGetLastError());
   RT_CUDA(cudaEventRecord(h->ev[1], st));
   reduce_tasks_kernel<<<static_cast<unsigned>(n_points), 32, 0, st>>>(
-      static_cast<double*>(h->partials.p), L.tpn, nb, d_sums);
+      static_cast<double*>(h->partials.p), L.tpn, nb, d_sums,
+      static_cast<unsigned long long*>(h->stats.p));
   RT_CUDA(cudaGetLastError());
   h->last_stream = st;
   h->have_timing = true;

@@ -1,0 +1,206 @@
+// rt_math.cuh — lean FP64 elementary functions for the tree walk.
+//
+// The arguments the method produces have known domains — log of a uniform in
+// (0,1), sinpi/cospi of 2v with v in (0,1), sqrt of a non-negative product,
+// 1/d with d >= 1, exp of a non-positive number — so the special-case
+// branches of general libm routines are unnecessary.  Accuracy target: a few
+// ulp (<= ~4e-16 relative, or ~1e-18 absolute near zero), far inside the
+// 1e-12 per-tree parity bound; checked against 64-bit-mantissa long double
+// references on the host (tests/test_math.py) and on the device.
+//
+// Polynomial coefficients live in the constant bank (RTM_CONST) so DFMA reads
+// them directly; the 2 KB log table is staged in shared memory by the kernel
+// (its index is lane-divergent).  Functions are __host__ __device__ so the
+// identical code is accuracy-tested on the CPU, where MUFU approximations are
+// emulated in FP32.
+#pragma once
+#include <cstdint>
+#include <cstring>
+#include <cmath>
+
+#include "rt_math_tables.h"
+
+#if defined(__CUDACC__)
+#define RTM_HD __host__ __device__ __forceinline__
+#else
+#define RTM_HD inline
+#endif
+
+namespace rtk {
+
+RTM_HD uint64_t dbits(double x) {
+#if defined(__CUDA_ARCH__)
+  return static_cast<uint64_t>(__double_as_longlong(x));
+#else
+  uint64_t u;
+  std::memcpy(&u, &x, 8);
+  return u;
+#endif
+}
+
+RTM_HD double dfrom(uint64_t u) {
+#if defined(__CUDA_ARCH__)
+  return __longlong_as_double(static_cast<long long>(u));
+#else
+  double x;
+  std::memcpy(&x, &u, 8);
+  return x;
+#endif
+}
+
+// MUFU.RCP64H / MUFU.RSQ64H seeds (~2^-22 relative); FP32 emulation on host.
+RTM_HD double rcp_seed(double x) {
+#if defined(__CUDA_ARCH__)
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+#else
+  return static_cast<double>(1.0f / static_cast<float>(x));
+#endif
+}
+
+RTM_HD double rsqrt_seed(double x) {
+#if defined(__CUDA_ARCH__)
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+#else
+  return static_cast<double>(1.0f / std::sqrt(static_cast<float>(x)));
+#endif
+}
+
+RTM_HD double rint_d(double x) {
+#if defined(__CUDA_ARCH__)
+  return rint(x);
+#else
+  return std::nearbyint(x);
+#endif
+}
+
+RTM_HD double fma_d(double a, double b, double c) {
+#if defined(__CUDA_ARCH__)
+  return fma(a, b, c);
+#else
+  return std::fma(a, b, c);
+#endif
+}
+
+// log(x) for positive normal x.  x = 2^k z, z ∈ [0.6875, 1.375); table entry
+// i (top 7 bits of bits(x) - bits(0.6875)) gives invc ≈ 1/c_i and
+// logc = -log(invc); r = z·invc − 1 (one rounding, |r| <= 2^-7);
+// log x = k ln2 + logc + r + r²·P(r).  11 FP64 ops + 1 I2F.
+RTM_HD double log_tab(double x, const LogEntry* T) {
+  const uint64_t ix = dbits(x);
+  const uint64_t tmp = ix - kLogOff;
+  const int i = static_cast<int>((tmp >> 45) & 127u);
+  const int64_t k = static_cast<int64_t>(tmp) >> 52;
+  const double z = dfrom(ix - (tmp & (0xfffull << 52)));
+  const LogEntry e = T[i];
+  const double r = fma_d(z, e.invc, -1.0);
+  double p = kLogP[6];
+  p = fma_d(p, r, kLogP[5]);
+  p = fma_d(p, r, kLogP[4]);
+  p = fma_d(p, r, kLogP[3]);
+  p = fma_d(p, r, kLogP[2]);
+  p = fma_d(p, r, kLogP[1]);
+  p = fma_d(p, r, kLogP[0]);
+  const double r2 = r * r;
+  const double t = fma_d(static_cast<double>(k), kLn2, e.logc);
+  return t + fma_d(r2, p, r);
+}
+
+// sin(pi f), cos(pi f) for |f| <= 1/4 (Taylor, remainders < 5e-17).
+RTM_HD void sincospi_core(double f, double& s, double& c) {
+  const double f2 = f * f;
+  double ps = kSinPi[7];
+  ps = fma_d(ps, f2, kSinPi[6]);
+  ps = fma_d(ps, f2, kSinPi[5]);
+  ps = fma_d(ps, f2, kSinPi[4]);
+  ps = fma_d(ps, f2, kSinPi[3]);
+  ps = fma_d(ps, f2, kSinPi[2]);
+  ps = fma_d(ps, f2, kSinPi[1]);
+  ps = fma_d(ps, f2, kSinPi[0]);
+  double pc = kCosPi[8];
+  pc = fma_d(pc, f2, kCosPi[7]);
+  pc = fma_d(pc, f2, kCosPi[6]);
+  pc = fma_d(pc, f2, kCosPi[5]);
+  pc = fma_d(pc, f2, kCosPi[4]);
+  pc = fma_d(pc, f2, kCosPi[3]);
+  pc = fma_d(pc, f2, kCosPi[2]);
+  pc = fma_d(pc, f2, kCosPi[1]);
+  s = ps * f;
+  c = fma_d(pc, f2, kCosPi[0]);
+}
+
+// sin(pi a), cos(pi a) for a ∈ [0, 2] on the 2^-52 grid (a = 2v, v = unif53):
+// q = rint(2a), f = a − q/2 exactly (|f| <= 1/4), rotate by q quarter turns.
+RTM_HD void sincospi2(double a, double& s_out, double& c_out) {
+  const double q = rint_d(2.0 * a);
+  const double f = fma_d(q, -0.5, a);
+  double s, c;
+  sincospi_core(f, s, c);
+  const int qi = static_cast<int>(q) & 3;
+  const bool swap = qi & 1;
+  double so = swap ? c : s;
+  double co = swap ? s : c;
+  const uint64_t sneg = (qi & 2) ? 0x8000000000000000ull : 0ull;
+  const uint64_t cneg = ((qi + 1) & 2) ? 0x8000000000000000ull : 0ull;
+  s_out = dfrom(dbits(so) ^ sneg);
+  c_out = dfrom(dbits(co) ^ cneg);
+}
+
+// cos(pi a) only (a as in sincospi2).
+RTM_HD double cospi2(double a) {
+  double s, c;
+  sincospi2(a, s, c);
+  return c;
+}
+
+// sqrt(a), a >= 0: rsqrt seed, one Newton step (2^-44), one Heron correction.
+RTM_HD double sqrt_nr(double a) {
+  double y = rsqrt_seed(a);
+  const double h = 0.5 * a;
+  const double t = h * y;
+  y = fma_d(y, fma_d(-t, y, 0.5), y);
+  double s = a * y;
+  const double r = fma_d(-s, s, a);
+  s = fma_d(r, 0.5 * y, s);
+  return a > 0.0 ? s : 0.0;
+}
+
+// 1/d for normal d > 0: rcp seed and one cubic correction y(1 + e + e²).
+RTM_HD double rcp_nr(double d) {
+  const double y = rcp_seed(d);
+  const double e = fma_d(-d, y, 1.0);
+  return fma_d(y, fma_d(e, e, e), y);
+}
+
+// exp(x) for x <= 0 (0 below -1075·ln2): x = k ln2 + r, |r| <= ln2/2, Taylor
+// degree 13, scaled by 2^k in two exact steps (subnormal results allowed).
+RTM_HD double exp_neg(double x) {
+  const double xc = x < -745.5 ? -745.5 : x;
+  const double kf = rint_d(xc * kLog2e);
+  double r = fma_d(kf, -kExpLn2Hi, xc);
+  r = fma_d(kf, -kExpLn2Lo, r);
+  double p = kExp[13];
+  p = fma_d(p, r, kExp[12]);
+  p = fma_d(p, r, kExp[11]);
+  p = fma_d(p, r, kExp[10]);
+  p = fma_d(p, r, kExp[9]);
+  p = fma_d(p, r, kExp[8]);
+  p = fma_d(p, r, kExp[7]);
+  p = fma_d(p, r, kExp[6]);
+  p = fma_d(p, r, kExp[5]);
+  p = fma_d(p, r, kExp[4]);
+  p = fma_d(p, r, kExp[3]);
+  p = fma_d(p, r, kExp[2]);
+  p = fma_d(p, r, kExp[1]);
+  p = fma_d(p, r, kExp[0]);
+  const int k = static_cast<int>(kf);
+  const int k1 = k / 2, k2 = k - k1;
+  const double s1 = dfrom(static_cast<uint64_t>(1023 + k1) << 52);
+  const double s2 = dfrom(static_cast<uint64_t>(1023 + k2) << 52);
+  return x < -745.5 ? 0.0 : (p * s1) * s2;
+}
+
+}  // namespace rtk

@@ -1,0 +1,97 @@
+"""Accuracy of the product's lean FP64 math (csrc/rt_math.cuh) on the host
+(same source; MUFU seeds emulated in FP32) against 64-bit-mantissa long-double
+references, over the argument domains the tree walk produces.
+The device build is checked the same way in tests/test_gpu_math.py."""
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+EPS = 2.0 ** -52
+
+
+@pytest.fixture(scope="module")
+def m(tmp_path_factory):
+    so = str(tmp_path_factory.mktemp("m") / "math_host.so")
+    subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fPIC", "-shared",
+                           os.path.join(HERE, "helpers", "math_host.cpp"), "-o", so])
+    lib = C.CDLL(so)
+    for f in ("m_log", "m_sqrt", "m_rcp", "m_exp"):
+        getattr(lib, f).argtypes = [C.c_void_p, C.c_long, C.c_void_p]
+    lib.m_sincospi2.argtypes = [C.c_void_p, C.c_long, C.c_void_p, C.c_void_p]
+    return lib
+
+
+def _u53(n, seed):
+    rng = np.random.default_rng(seed)
+    m = rng.integers(0, 2 ** 52, size=n, dtype=np.uint64)
+    return (2 * m + 1).astype(np.float64) * 2.0 ** -53
+
+
+def _call(lib, name, x):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    getattr(lib, name)(x.ctypes.data, x.size, y.ctypes.data)
+    return y
+
+
+def test_log_unit_interval(m):
+    x = np.concatenate([_u53(400_000, 1), [2.0 ** -53, 1 - 2.0 ** -53, 0.5, 0.6875, 1 - 2.0 ** -30,
+                                           0.68749999999999989, 0.99609375, 0.70710678118654757]])
+    got = _call(m, "m_log", x)
+    ref = np.log(x.astype(np.longdouble))
+    err = np.abs(got.astype(np.longdouble) - ref)
+    rel = err / np.abs(ref)
+    assert float(np.max(rel)) < 4 * EPS, float(np.max(rel))
+    # general positive normals too (the routine is not specific to (0,1))
+    y = np.exp(np.random.default_rng(2).uniform(-700, 700, 100_000))
+    g = _call(m, "m_log", y)
+    r = np.log(y.astype(np.longdouble))
+    assert float(np.max(np.abs(g - r) / np.maximum(np.abs(r), 1e-300))) < 4 * EPS
+
+
+def test_log_near_one_relative(m):
+    """log(1 - 2^-k) keeps relative accuracy (the table entries at 1 are exact)."""
+    x = 1.0 - 2.0 ** -np.arange(8, 53, dtype=np.float64)
+    got = _call(m, "m_log", x)
+    ref = np.log1p(-(2.0 ** -np.arange(8, 53)).astype(np.longdouble))
+    assert float(np.max(np.abs(got - ref) / np.abs(ref))) < 4 * EPS
+
+
+def test_sincospi2(m):
+    a = np.concatenate([2 * _u53(400_000, 3), [0.0, 0.25, 0.5, 0.75, 1.0, 1.25, 1.5, 1.75, 2.0]])
+    s = np.empty_like(a); c = np.empty_like(a)
+    m.m_sincospi2(a.ctypes.data, a.size, s.ctypes.data, c.ctypes.data)
+    pi = np.longdouble("3.14159265358979323846264338327950288")
+    sr = np.sin(pi * a.astype(np.longdouble)); cr = np.cos(pi * a.astype(np.longdouble))
+    assert float(np.max(np.abs(s - sr))) < 2.5 * EPS / 2
+    assert float(np.max(np.abs(c - cr))) < 2.5 * EPS / 2
+    # exact values at the quadrant points a = 0, 1/2, 1, 3/2, 2
+    assert (s[-9], c[-9]) == (0.0, 1.0) and (s[-7], c[-7]) == (1.0, 0.0)
+    assert (s[-5], c[-5]) == (0.0, -1.0) and (s[-3], c[-3]) == (-1.0, 0.0)
+    assert (s[-1], c[-1]) == (0.0, 1.0)
+
+
+def test_sqrt_rcp(m):
+    rng = np.random.default_rng(4)
+    x = np.concatenate([np.exp(rng.uniform(-80, 80, 300_000)), [0.0, 1.0, 4.0, 2.0 ** -60]])
+    got = _call(m, "m_sqrt", x)
+    ref = np.sqrt(x.astype(np.longdouble))
+    rel = np.abs(got - ref) / np.maximum(ref, 1e-300)
+    assert float(np.max(rel)) < 2 * EPS and got[-4] == 0.0
+    d = 1.0 + np.exp(rng.uniform(-40, 20, 300_000))
+    got = _call(m, "m_rcp", d)
+    ref = 1 / d.astype(np.longdouble)
+    assert float(np.max(np.abs(got - ref) / ref)) < 2 * EPS
+
+
+def test_exp_neg(m):
+    rng = np.random.default_rng(5)
+    x = np.concatenate([-rng.exponential(3.0, 300_000), -rng.uniform(0, 700, 50_000), [0.0, -1e-300, -708.0]])
+    got = _call(m, "m_exp", x)
+    ref = np.exp(x.astype(np.longdouble))
+    assert float(np.max(np.abs(got - ref) / ref)) < 4 * EPS
+    assert _call(m, "m_exp", np.array([-800.0]))[0] == 0.0
