@@ -37,30 +37,40 @@ import workloads as W  # noqa: E402
 # (MEASURED_PEAKS.json sm_max_mhz; /opt/skills/guides/B200_PROFILING.md).
 N_SM, FP64_LANES, F_MAX_MHZ = 148, 64, 1965.0
 
-# Algorithmic FP64 lane-instructions per operation of the method (DESIGN.md
-# §5): the FP64 instructions CUDA's own libdevice routines issue on their
-# fast path (SASS counts of DFMA/DMUL/DADD/DSETP/DMNMX/F2F.F64 per call),
-# plus the method's plain arithmetic.
-COST = dict(log=26, sqrt=9, sincospi=28, cospi=17, exp=19, tanh=27, rcp_div=9, unif=1)
+# Algorithmic FP64 work: the method written plainly — as the
+# oracle does, S = -log(U)/λ, x' = y + σ sqrt(h) ξ with textbook Box–Muller —
+# costed with the FP64-pipe instructions CUDA's own libdevice routines issue
+# on their main path (tools/libdevice_costs.py: CUDA 12.9, sm_100a), plus one
+# per plain add/mul/fma/compare.  The kernel's own cheaper math therefore
+# raises the achieved rate; it cannot inflate the count.
+LD = dict(log=30, exp=18, sqrt=8, div=8, tanh=37, sincospi=25, cospi=16, u2d=1)
+
+
+def algo_fp64_per_unit(eq: dict) -> dict:
+    d = eq["dim"]
+    unif = LD["u2d"] + 1                                   # (double)m * 2^-53
+    pair_both = 2 * unif + LD["log"] + 1 + LD["sqrt"] + 1 + LD["sincospi"] + 2
+    pair_cos = 2 * unif + LD["log"] + 1 + LD["sqrt"] + 1 + LD["cospi"] + 1
+    per_particle = (unif + LD["log"] + 1        # S = -log(U) * (1/λ)
+                    + 1                          # S > τ
+                    + LD["sqrt"] + 1             # σ sqrt(h)
+                    + d)                         # y_k + (σ√h) ξ_k
+    per_particle += {1: pair_cos, 2: pair_both, 3: pair_both + pair_cos}[d]
+    r2 = 2 * d - 1
+    g = {W.G_CONST: 0,
+         W.G_TANH_STEP: LD["div"] + LD["tanh"] + 1 + 2,
+         W.G_GAUSS: r2 + LD["div"] + LD["exp"] + 1,
+         W.G_LORENTZ: r2 + LD["div"] + 1 + LD["div"]}[eq["init_kind"]]
+    return dict(particle=per_particle, leaf=g + 1,   # Π *= g
+                split=2,                             # Π *= w_k, τ − S
+                tree=3)                              # C², ΣC, ΣC²
 
 
 def algo_fp64_ops(eq: dict, stats: dict) -> float:
     """Algorithmic FP64 lane-ops of one launch from its event counters."""
-    d = eq["dim"]
-    parts, leaves, splits, trees = stats["particles"], stats["leaves"], stats["splits"], stats["trees"]
-    # per particle: U_S (unif + log + mul), compare, Box–Muller pair(s)
-    # (2 unif, log, mul, sqrt, sincospi, 2 mul), sqrt(h), sigma*sqrt, d FMA
-    bm_pairs = 1 if d <= 2 else 2
-    per_particle = (COST["unif"] + COST["log"] + 1 + 1 +
-                    bm_pairs * (2 * COST["unif"] + COST["log"] + 1 + COST["sqrt"] + 2)
-                    + (COST["sincospi"] if True else 0) + (COST["cospi"] if d == 3 else 0)
-                    + COST["sqrt"] + 1 + d)
-    g = {W.G_CONST: 0, W.G_TANH_STEP: COST["tanh"] + 3, W.G_GAUSS: COST["exp"] + 2 + 2 * (d - 1),
-         W.G_LORENTZ: COST["rcp_div"] + 2 + 2 * (d - 1)}[eq["init_kind"]]
-    per_leaf = g + 1
-    per_split = 2          # Π *= w_k, τ − S
-    per_tree = 2           # ΣC += C, ΣC² = fma(C, C, ΣC²)
-    return parts * per_particle + leaves * per_leaf + splits * per_split + trees * per_tree
+    u = algo_fp64_per_unit(eq)
+    return (stats["particles"] * u["particle"] + stats["leaves"] * u["leaf"] +
+            stats["splits"] * u["split"] + stats["trees"] * u["tree"])
 
 
 class ClockSampler:
@@ -214,10 +224,12 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
     stream = torch.cuda.current_stream()
 
+    from paper_2402_06491_b200.dist import merge_sums, tree_range
+    off, n_rank = tree_range(rank, ws, N)
+
     def step():
-        est.sums(x, t, N, seed, tree_offset=rank * N, out=sums)
-        if dist is not None:
-            dist.all_reduce(sums)
+        est.sums(x, t, n_rank, seed, tree_offset=off, out=sums)
+        merge_sums(sums)                     # one all-reduce of (K+2)x3 doubles per node
         c, se, us, ses = P.finalize(sums, K, N * ws)
         u, fl = P.pade(c, L, M)
         return u, ses
