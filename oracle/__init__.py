@@ -67,6 +67,8 @@ def lib():
         _lib.or_philox.argtypes = [C.POINTER(C.c_uint32)] * 3
         _lib.or_unif53.argtypes = [C.c_uint32, C.c_uint32]
         _lib.or_unif53.restype = C.c_double
+        _lib.or_unif32.argtypes = [C.c_uint32]
+        _lib.or_unif32.restype = C.c_double
         _lib.or_normalize.argtypes = [C.POINTER(Params), C.POINTER(Norm)]
         _lib.or_tree.argtypes = [C.POINTER(Params), dp, C.c_int64, C.c_int64, C.c_double,
                                  C.c_uint64, C.POINTER(TreeRec)]
@@ -107,6 +109,10 @@ def philox(key, ctr) -> np.ndarray:
 
 def unif53(lo: int, hi: int) -> float:
     return lib().or_unif53(lo, hi)
+
+
+def unif32(w: int) -> float:
+    return lib().or_unif32(w)
 
 
 def normalize(eq: dict) -> dict:

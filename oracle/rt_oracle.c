@@ -49,6 +49,11 @@ double or_unif53(uint32_t lo, uint32_t hi) {
   return (double)m * 0x1.0p-53;
 }
 
+/* Uniform in (0,1) from 32 random bits: (2w+1) * 2^-33 (exact). */
+double or_unif32(uint32_t w) {
+  return (2.0 * (double)w + 1.0) * 0x1.0p-33;
+}
+
 static void draw(uint64_t seed, int64_t i, int64_t j, uint64_t label, uint32_t call,
                  uint32_t out[4]) {
   uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
@@ -143,27 +148,36 @@ typedef struct {
 static double particle(tree_ctx* c, const double* y, double tau, uint64_t label) {
   const or_params* p = c->p;
   const or_norm* nz = c->nz;
-  uint32_t r0[4], r1[4], r2[4];
+  uint32_t r0[4], r1[4];
   c->particles++;
   draw(c->seed, c->i, c->j, label, 0, r0);
   draw(c->seed, c->i, c->j, label, 1, r1);
-  if (p->dim == 3) draw(c->seed, c->i, c->j, label, 2, r2);
 
   /* exponential clock S with density λ e^{-λS} */
   double S = -log(or_unif53(r0[0], r0[1])) * nz->inv_lambda;
 
   /* Brownian increment over the particle's lifetime (Eqs. green, SDE,
-   * PAPER.md:174-191): textbook Box–Muller normals.                      */
+   * PAPER.md:174-191): textbook Box–Muller normals.  d <= 2: one pair from
+   * block 1 (radius uniform w1:w0, angle uniform w3:w2).  d = 3 (DESIGN.md
+   * R8): two pairs from the same two blocks — radii from block-1 words
+   * (w1:w0) and (w3:w2), angles from 32-bit uniforms: block-0 word 3, and the
+   * word assembled from the 12 low bits the 53-bit uniforms leave unused
+   * (block-0 w0, block-1 w0, block-1 w2).                               */
   double xi[3];
-  {
+  if (p->dim <= 2) {
     double v1 = or_unif53(r1[0], r1[1]), v2 = or_unif53(r1[2], r1[3]);
     double rr = sqrt(-2.0 * log(v1));
     xi[0] = rr * cos(2.0 * M_PI * v2);
     xi[1] = rr * sin(2.0 * M_PI * v2);
-    if (p->dim == 3) {
-      double v3 = or_unif53(r2[0], r2[1]), v4 = or_unif53(r2[2], r2[3]);
-      xi[2] = sqrt(-2.0 * log(v3)) * cos(2.0 * M_PI * v4);
-    }
+  } else {
+    double v1 = or_unif53(r1[0], r1[1]), v2 = or_unif32(r0[3]);
+    double v3 = or_unif53(r1[2], r1[3]);
+    uint32_t w4 = ((r0[0] & 0xFFFu) << 20) | ((r1[0] & 0xFFFu) << 8) | ((r1[2] & 0xFFFu) >> 4);
+    double v4 = or_unif32(w4);
+    double rr = sqrt(-2.0 * log(v1));
+    xi[0] = rr * cos(2.0 * M_PI * v2);
+    xi[1] = rr * sin(2.0 * M_PI * v2);
+    xi[2] = sqrt(-2.0 * log(v3)) * cos(2.0 * M_PI * v4);
   }
   double h = (S > tau) ? tau : S;
   double step = nz->sigma * sqrt(h);

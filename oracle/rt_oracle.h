@@ -58,6 +58,8 @@ typedef struct { int64_t trees, pruned, particles, leaves, splits; } or_stats;
 void or_philox(const uint32_t key[2], const uint32_t ctr[4], uint32_t out[4]);
 /* (2*(x>>12)+1) * 2^-53 */
 double or_unif53(uint32_t lo, uint32_t hi);
+/* (2w+1) * 2^-33 */
+double or_unif32(uint32_t w);
 
 int or_normalize(const or_params* p, or_norm* out);   /* 0 ok, else error */
 

@@ -18,8 +18,8 @@
 // remaining count << 56).
 //
 // Order binning: a finished tree appends
-// (bin, C) to its task slot's 64-entry per-warp ring in shared memory and
-// bumps the slot's integer bin count (shared atomic: exact in any order);
+// (bin | task slot << 5, C) to a 64-entry per-warp ring in shared memory and
+// bumps its slot's integer bin count (shared atomic: exact in any order);
 // when 32 records are pending the warp "transposes" them: lane b owns order
 // bin b and accumulates, in ring order, the records whose bin is b (ΣC, ΣC²;
 // deterministic).  When all trees of a task are recorded, lane b writes the
@@ -38,8 +38,9 @@ constexpr int kWarpsPerCta = 4;
 constexpr int kThreads = 32 * kWarpsPerCta;
 constexpr int kRing = 64;
 constexpr uint64_t kLabelMask = (1ull << 56) - 1;
-// per-warp record rings [2 slots][kRing] (C, bin), bin sums [2][2][32], counts [2][32]
-constexpr int kWarpExtra = 2 * kRing * 8 + 2 * 2 * 32 * 8 + 2 * kRing * 4 + 2 * 32 * 4;
+// per-warp record ring [kRing] (C, bin | slot << 5), bin sums [2 slots][2][32],
+// counts [2][32]; the ring is flushed completely once >= 32 records are pending
+constexpr int kWarpExtra = kRing * 8 + 2 * 2 * 32 * 8 + kRing * 4 + 2 * 32 * 4;
 
 // Stack levels kept in shared memory per lane, and resident CTAs per SM (the
 // register budget 65536 / (128 v) and the 228 KB of shared memory).  The
@@ -48,9 +49,9 @@ constexpr int kWarpExtra = 2 * kRing * 8 + 2 * 2 * 32 * 8 + 2 * kRing * 4 + 2 * 
 template <int DIM> struct Levels;
 template <> struct Levels<1> { static constexpr int v = 7; };
 template <> struct Levels<2> { static constexpr int v = 5; };
-template <> struct Levels<3> { static constexpr int v = 6; };
+template <> struct Levels<3> { static constexpr int v = 5; };
 template <int DIM, bool REC> struct MinCtas {
-  static constexpr int v = (DIM == 3 ? 5 : 6) - (REC ? 1 : 0);
+  static constexpr int v = (DIM == 3 ? 6 : 7) - (REC ? 1 : 0);
 };
 
 struct TreeRec {   // mirrors rt_tree_rec
@@ -118,9 +119,9 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   unsigned char* const wbase = smem_raw + 128 * 16 + wib * (stack_bytes_per_warp<DIM>() + kWarpExtra);
   double* const ssp = reinterpret_cast<double*>(wbase) + lane;            // [LV][NF][32]
   double* const ringC = reinterpret_cast<double*>(wbase + stack_bytes_per_warp<DIM>());
-  double* const bsum = ringC + 2 * kRing;                                 // [slot][ΣC, ΣC²][32]
-  int* const ringBin = reinterpret_cast<int*>(bsum + 2 * 2 * 32);         // [slot][kRing]
-  int* const bcnt = ringBin + 2 * kRing;                                  // [slot][32]
+  double* const bsum = ringC + kRing;                                     // [slot][ΣC, ΣC²][32]
+  int* const ringBin = reinterpret_cast<int*>(bsum + 2 * 2 * 32);         // [kRing]
+  int* const bcnt = ringBin + kRing;                                      // [slot][32]
   double* const wtab = reinterpret_cast<double*>(smem_raw + 128 * 16 +
       kWarpsPerCta * (stack_bytes_per_warp<DIM>() + kWarpExtra));        // [9] weights
   int* const ktab = reinterpret_cast<int*>(wtab + 9);                     // [9] offspring k
@@ -160,7 +161,8 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   if (!stream_end) open_task(iss_task);
   int slot_task0 = stream_end ? -1 : iss_task, slot_task1 = -1;
   int slot_left0 = iss_size, slot_left1 = 0;
-  int ring_head0 = 0, ring_cnt0 = 0, ring_head1 = 0, ring_cnt1 = 0;
+  int ring_cnt = 0;    // pending records (always flushed completely)
+  int ring_mask = 0;   // bit s: some pending record belongs to task slot s
 
   // ---- lane state ----------------------------------------------------------
   bool active = false;
@@ -221,27 +223,36 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     // Box–Muller with the lifetime folded into the radius (R8):
     // σ sqrt(h) · sqrt(-2 log v1) · (cos, sin)(2π v2)
     double x[DIM];
-    {
+    if constexpr (DIM <= 2) {
       const double v1 = unif53(r1.x, r1.y), v2 = unif53(r1.z, r1.w);
       const double rad = sqrt_nr(-2.0 * log_tab(v1, ltab) * h2d);
       double sn, cs;
       sincospi2(2.0 * v2, sn, cs);
       x[0] = fma(rad, cs, y[0]);
       if constexpr (DIM >= 2) x[1] = fma(rad, sn, y[1]);
-    }
-    if constexpr (DIM == 3) {
-      const uint4 r2 = philox4x32_10(tj, ti, c2, c3 | (2u << 24), P.rk);
-      const double v3 = unif53(r2.x, r2.y), v4 = unif53(r2.z, r2.w);
+    } else {
+      // d = 3 from the same two blocks (R8): radii uniforms from
+      // block-1 (w1:w0), (w3:w2); angles from 32-bit uniforms — block-0 w3 and
+      // the word of the 12 low bits the 53-bit uniforms leave unused
+      const double v1 = unif53(r1.x, r1.y), v2 = unif32(r0.w);
+      const double v3 = unif53(r1.z, r1.w);
+      const uint32_t w4 = ((r0.x & 0xFFFu) << 20) | ((r1.x & 0xFFFu) << 8) | ((r1.z & 0xFFFu) >> 4);
+      const double v4 = unif32(w4);
+      const double rad = sqrt_nr(-2.0 * log_tab(v1, ltab) * h2d);
+      double sn, cs;
+      sincospi2(2.0 * v2, sn, cs);
+      x[0] = fma(rad, cs, y[0]);
+      x[1] = fma(rad, sn, y[1]);
       const double rad2 = sqrt_nr(-2.0 * log_tab(v3, ltab) * h2d);
       x[2] = fma(rad2, cospi2(2.0 * v4), y[2]);
     }
     // categorical offspring choice from the integer thresholds (R9)
+    // (thresholds past the support are 0xffffffff, so the sum needs no bound)
     const uint32_t c32 = r0.z;
-    int s = 0;
+    int s = (c32 > P.thr[0]) + (c32 > P.thr[1]) + (c32 > P.thr[2]) + (c32 > P.thr[3]);
+    if (P.n_support > 5) {                      // warp-uniform, rare
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      if (q + 1 >= P.n_support) break;          // warp-uniform (kernel parameter)
-      s += (c32 > P.thr[q]) ? 1 : 0;
+      for (int q = 4; q < 8; ++q) s += (c32 > P.thr[q]) ? 1 : 0;
     }
     const double gv = g_eval<DIM, GK>(x, P);    // g at the leaf
     const int k = ktab[s];
@@ -262,57 +273,63 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       parts += active ? 1 : 0;
       leaves += (active && leaf) ? 1 : 0;
     }
-    const bool child = branch && k > 0;          // continue with child 0
-    const bool push = child && k > 1;            // k-1 younger siblings wait
+    const bool push = branch && k > 1;           // k-1 younger siblings wait
     const bool pop = (active && leaf) || (branch && k == 0);
     const double tc = tau - S;
     const uint64_t base = label << P.beta;
-    if (push) {
-      const uint64_t pk = (base | 1ull) | (static_cast<uint64_t>(k - 1) << 56);
-      if (sp < LV) {
+    // push the younger siblings: shared-memory levels inline, the rare deep
+    // levels (global) behind a warp-uniform test so they cost nothing otherwise
+    const uint64_t push_pk = (base | 1ull) | (static_cast<uint64_t>(k - 1) << 56);
+    if (push && sp < LV) {
 #pragma unroll
-        for (int q = 0; q < DIM; ++q) ssp[(sp * NF + q) * 32] = x[q];
-        ssp[(sp * NF + DIM) * 32] = tc;
-        ssp[(sp * NF + DIM + 1) * 32] = __longlong_as_double(static_cast<long long>(pk));
-      } else {
+      for (int q = 0; q < DIM; ++q) ssp[(sp * NF + q) * 32] = x[q];
+      ssp[(sp * NF + DIM) * 32] = tc;
+      ssp[(sp * NF + DIM + 1) * 32] = __longlong_as_double(static_cast<long long>(push_pk));
+    }
+    if (__any_sync(0xffffffffu, push && sp >= LV)) {
+      if (push && sp >= LV) {
         double* b = gsp + (sp - LV) * (NF * 32);
 #pragma unroll
         for (int q = 0; q < DIM; ++q) b[q * 32] = x[q];
         b[DIM * 32] = tc;
-        b[(DIM + 1) * 32] = __longlong_as_double(static_cast<long long>(pk));
+        b[(DIM + 1) * 32] = __longlong_as_double(static_cast<long long>(push_pk));
       }
-      ++sp;
     }
-    if (child) {
+    sp += push ? 1 : 0;
+    // continue with child 0 (lanes that pop overwrite this below; lanes whose
+    // tree ended are re-initialised at assignment)
 #pragma unroll
-      for (int q = 0; q < DIM; ++q) y[q] = x[q];
-      tau = tc;
-      label = base;
+    for (int q = 0; q < DIM; ++q) y[q] = x[q];
+    tau = tc;
+    label = base;
+    const bool done = pruned || kill || (pop && sp == 0);
+    const int lvl = sp - 1;
+    const bool pop_s = pop && sp > 0 && lvl < LV;
+    uint64_t pk = 0;
+    if (pop_s) {
+#pragma unroll
+      for (int q = 0; q < DIM; ++q) y[q] = ssp[(lvl * NF + q) * 32];
+      tau = ssp[(lvl * NF + DIM) * 32];
+      pk = static_cast<uint64_t>(__double_as_longlong(ssp[(lvl * NF + DIM + 1) * 32]));
     }
-    bool done = pruned || kill || (pop && sp == 0);
-    if (pop && sp > 0) {
-      const int lvl = sp - 1;
-      uint64_t pk;
-      if (lvl < LV) {
-#pragma unroll
-        for (int q = 0; q < DIM; ++q) y[q] = ssp[(lvl * NF + q) * 32];
-        tau = ssp[(lvl * NF + DIM) * 32];
-        pk = static_cast<uint64_t>(__double_as_longlong(ssp[(lvl * NF + DIM + 1) * 32]));
-      } else {
+    if (__any_sync(0xffffffffu, pop && lvl >= LV)) {
+      if (pop && lvl >= LV) {
         const double* b = gsp + (lvl - LV) * (NF * 32);
 #pragma unroll
         for (int q = 0; q < DIM; ++q) y[q] = b[q * 32];
         tau = b[DIM * 32];
         pk = static_cast<uint64_t>(__double_as_longlong(b[(DIM + 1) * 32]));
+        if ((pk >> 56) != 1ull)
+          gsp[((lvl - LV) * NF + DIM + 1) * 32] =
+              __longlong_as_double(static_cast<long long>(pk + 1ull - (1ull << 56)));
       }
+    }
+    if (pop && sp > 0) {
       label = pk & kLabelMask;
-      if ((pk >> 56) == 1ull) {
-        sp = lvl;                               // last sibling: drop the group
-      } else {
-        const double npk = __longlong_as_double(static_cast<long long>(pk + 1ull - (1ull << 56)));
-        if (lvl < LV) ssp[(lvl * NF + DIM + 1) * 32] = npk;
-        else gsp[((lvl - LV) * NF + DIM + 1) * 32] = npk;
-      }
+      if ((pk >> 56) == 1ull) sp = lvl;         // last sibling: drop the group
+      else if (lvl < LV)
+        ssp[(lvl * NF + DIM + 1) * 32] =
+            __longlong_as_double(static_cast<long long>(pk + 1ull - (1ull << 56)));
     }
 
     if constexpr (REC) {
@@ -332,43 +349,64 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       const unsigned fin0 = fin & ~fin1;
       if (done) {
         const int bin = pruned ? (P.K + 1) : ne;
-        const int e = slot ? (ring_head1 + ring_cnt1 + __popc(fin1 & lt_mask)) & (kRing - 1)
-                           : (ring_head0 + ring_cnt0 + __popc(fin0 & lt_mask)) & (kRing - 1);
-        ringBin[slot * kRing + e] = bin;
-        ringC[slot * kRing + e] = pruned ? 0.0 : Pi;
+        const int e = ring_cnt + __popc(fin & lt_mask);
+        ringBin[e] = bin | (slot << 5);
+        ringC[e] = pruned ? 0.0 : Pi;
         atomicAdd(bcnt + slot * 32 + bin, 1);   // integer: exact in any order
         active = false;
       }
-      ring_cnt0 += __popc(fin0);
-      ring_cnt1 += __popc(fin1);
+      ring_cnt += __popc(fin);
+      ring_mask |= (fin1 ? 2 : 0) | (fin0 ? 1 : 0);
       slot_left0 -= __popc(fin0);
       slot_left1 -= __popc(fin1);
       __syncwarp();
       const bool cl0 = slot_task0 >= 0 && slot_left0 == 0;
       const bool cl1 = slot_task1 >= 0 && slot_left1 == 0;
-#pragma unroll
-      for (int sl = 0; sl < 2; ++sl) {
-        const bool close = sl ? cl1 : cl0;
-        int& head = sl ? ring_head1 : ring_head0;
-        int& cnt = sl ? ring_cnt1 : ring_cnt0;
-        if (close || cnt >= 32) {
-          // transpose: lane b accumulates, in ring order, the records of bin b
-          const int nflush = close ? cnt : 32;
+      if (cl0 || cl1 || ring_cnt >= 32) {
+        // transpose all pending records: lane b accumulates, in ring order, the
+        // records of bin b (one slot in the common case, both near task ends)
+        if (ring_mask != 3) {
+          const int sl = ring_mask >> 1;
           double a1 = bsum[(sl * 2 + 0) * 32 + lane], a2 = bsum[(sl * 2 + 1) * 32 + lane];
-          const int* rb = ringBin + sl * kRing;
-          const double* rc = ringC + sl * kRing;
-          for (int r = 0; r < nflush; ++r) {
-            const int e = (head + r) & (kRing - 1);
-            const int b = rb[e];
-            const double C = rc[e];
-            if (b == lane) {
+          const int code = lane | (sl << 5);
+          for (int r = 0; r < ring_cnt; ++r) {
+            const int b = ringBin[r];
+            const double C = ringC[r];
+            if (b == code) {
               a1 += C;
               a2 = fma(C, C, a2);
             }
           }
-          head = (head + nflush) & (kRing - 1);
-          cnt -= nflush;
-          if (close) {
+          bsum[(sl * 2 + 0) * 32 + lane] = a1;
+          bsum[(sl * 2 + 1) * 32 + lane] = a2;
+        } else {
+          double a1 = bsum[lane], a2 = bsum[32 + lane];
+          double b1 = bsum[64 + lane], b2 = bsum[96 + lane];
+          for (int r = 0; r < ring_cnt; ++r) {
+            const int b = ringBin[r];
+            const double C = ringC[r];
+            if (b == lane) {
+              a1 += C;
+              a2 = fma(C, C, a2);
+            }
+            if (b == (lane | 32)) {
+              b1 += C;
+              b2 = fma(C, C, b2);
+            }
+          }
+          bsum[lane] = a1; bsum[32 + lane] = a2;
+          bsum[64 + lane] = b1; bsum[96 + lane] = b2;
+        }
+        ring_cnt = 0;
+        ring_mask = 0;
+        __syncwarp();
+      }
+#pragma unroll
+      for (int sl = 0; sl < 2; ++sl) {
+        const bool close = sl ? cl1 : cl0;
+        if (close) {
+          double a1 = bsum[(sl * 2 + 0) * 32 + lane], a2 = bsum[(sl * 2 + 1) * 32 + lane];
+          {
             const int task = sl ? slot_task1 : slot_task0;
             if (lane < P.nb) {
               double* o = P.partials + (static_cast<int64_t>(task) * P.nb + lane) * 3;

@@ -65,6 +65,13 @@ def test_unif53_exact(orc):
     assert 0.0 < orc.unif53(0, 0) < orc.unif53(0xFFFFFFFF, 0xFFFFFFFF) < 1.0
 
 
+def test_unif32_exact(orc):
+    """32-bit uniforms (the d = 3 Box–Muller angles, R8): (2w+1)/2^33."""
+    assert orc.unif32(0) == 2.0 ** -33
+    assert orc.unif32(0xFFFFFFFF) == 1.0 - 2.0 ** -33
+    assert orc.unif32(12345) == (2 * 12345 + 1) / 2.0 ** 33
+
+
 def test_root_particle_laws(orc):
     """Root lifetime S ~ Exp(λ) and Gaussian displacement over min(S, t).
 
