@@ -159,8 +159,10 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 #pragma unroll
   for (int k = 0; k < DIM; ++k) iss_y[k] = 0.0;
   if (!stream_end) open_task(iss_task);
+  // per task slot: task id and trees not yet recorded (kFree: slot unused)
+  constexpr int kFree = -(1 << 30);
   int slot_task0 = stream_end ? -1 : iss_task, slot_task1 = -1;
-  int slot_left0 = iss_size, slot_left1 = 0;
+  int slot_left0 = stream_end ? kFree : iss_size, slot_left1 = kFree;
   int ring_cnt = 0;    // pending records (always flushed completely)
   int ring_mask = 0;   // bit s: some pending record belongs to task slot s
 
@@ -177,8 +179,10 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   int leaves = 0, parts = 0;           // per-tree counts (trace variant only)
   uint32_t c_part = 0u, c_leaf = 0u;   // particles / leaves since the last task close
 
-  while (true) {
-    // ---------------- assign trees to idle lanes (warp-uniform control) -----
+  // Hand the next trees of the warp's stream to idle lanes (warp-uniform).
+  // Lanes only become idle when trees finish, so this runs at start-up and
+  // after a tree-completion event.
+  auto assign = [&]() {
     unsigned idle = __ballot_sync(0xffffffffu, !active);
     while (idle != 0u && !stream_end) {
       const int avail = iss_size - iss_next;
@@ -186,7 +190,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
         const int nt = iss_task + W;
         if (nt >= P.n_tasks) { stream_end = true; break; }
         const int ns = iss_slot ^ 1;
-        if ((ns == 0 ? slot_task0 : slot_task1) != -1) break;   // previous task still open
+        if ((ns == 0 ? slot_left0 : slot_left1) != kFree) break;   // previous task still open
         iss_task = nt; iss_next = 0; iss_slot = ns;
         open_task(nt);
         if (ns == 0) { slot_task0 = nt; slot_left0 = iss_size; }
@@ -209,7 +213,13 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       iss_next += take;
       idle = __ballot_sync(0xffffffffu, !active);
     }
-    if (!__any_sync(0xffffffffu, active)) break;
+  };
+  assign();
+
+  while (true) {
+    if (stream_end) {                                  // warp-uniform
+      if (!__any_sync(0xffffffffu, active)) break;
+    }
 
     // ---------------- one particle per lane (converged) ----------------------
     const uint32_t c2 = static_cast<uint32_t>(label);
@@ -355,13 +365,14 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
         atomicAdd(bcnt + slot * 32 + bin, 1);   // integer: exact in any order
         active = false;
       }
-      ring_cnt += __popc(fin);
-      ring_mask |= (fin1 ? 2 : 0) | (fin0 ? 1 : 0);
-      slot_left0 -= __popc(fin0);
-      slot_left1 -= __popc(fin1);
+      const int n1 = __popc(fin1), n0 = __popc(fin) - n1;
+      ring_cnt += n0 + n1;
+      ring_mask |= (n1 ? 2 : 0) | (n0 ? 1 : 0);
+      slot_left0 -= n0;
+      slot_left1 -= n1;
       __syncwarp();
-      const bool cl0 = slot_task0 >= 0 && slot_left0 == 0;
-      const bool cl1 = slot_task1 >= 0 && slot_left1 == 0;
+      const bool cl0 = slot_left0 == 0;
+      const bool cl1 = slot_left1 == 0;
       if (cl0 || cl1 || ring_cnt >= 32) {
         // transpose all pending records: lane b accumulates, in ring order, the
         // records of bin b (one slot in the common case, both near task ends)
@@ -414,7 +425,8 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
             }
             bcnt[sl * 32 + lane] = 0;
             a1 = 0.0; a2 = 0.0;
-            if (sl) slot_task1 = -1; else slot_task0 = -1;
+            if (sl) { slot_task1 = -1; slot_left1 = kFree; }
+            else { slot_task0 = -1; slot_left0 = kFree; }
             // fold the lanes' 32-bit event counters into the 64-bit totals
             unsigned long long v0 = c_part, v1 = c_leaf;
 #pragma unroll
@@ -434,6 +446,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
           __syncwarp();
         }
       }
+      assign();                                // finished lanes take new trees
     }
   }
   // (trees, pruned trees and splits follow exactly from the bin counts and are
