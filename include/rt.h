@@ -193,6 +193,12 @@ rt_status rt_get_stats(const rt_handle* h, rt_stats* out);
  * and trees per task.  Changes only summation order. */
 rt_status rt_set_launch(rt_handle* h, int32_t grid_ctas, int64_t trees_per_task);
 
+/* Stack-pool override (0 = automatic): at most pool_entries pending sibling
+ * groups per warp are kept in shared memory, the rest in the global overflow
+ * area.  Changes neither results nor summation order; tests use
+ * it to exercise the overflow path.  RT_E_ARG: null handle, pool_entries < 0. */
+rt_status rt_set_pool(rt_handle* h, int32_t pool_entries);
+
 /* The library's Philox4x32-10 block function on device buffers:
  * d_out[4q..4q+3] = philox(key, d_ctr[4q..4q+3]), q < n (RNG parity tests). */
 rt_status rt_philox_dev(uint64_t key, const uint32_t* d_ctr, int64_t n, uint32_t* d_out,

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 #include <string>
@@ -83,9 +84,10 @@ struct rt_handle {
   cudaStream_t last_stream = nullptr;
   bool have_timing = false;
   double host_total_ms = -1.0;
-  DevBuf partials, spill, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
+  DevBuf partials, gpool, gaux, wtime, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
   int32_t grid_override = 0;
   int64_t tpt_override = 0;
+  int32_t pool_override = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -185,7 +187,7 @@ extern "C" rt_status rt_destroy(rt_handle* h) {
   if (!h) return RT_OK;
   if (h->own_stream) cudaStreamSynchronize(h->own_stream);
   if (h->last_stream) cudaStreamSynchronize(h->last_stream);
-  for (DevBuf* b : {&h->partials, &h->spill, &h->sums, &h->stats, &h->h_points, &h->h_coeffs,
+  for (DevBuf* b : {&h->partials, &h->gpool, &h->gaux, &h->wtime, &h->sums, &h->stats, &h->h_points, &h->h_coeffs,
                     &h->h_stderr, &h->h_aux, &h->h_flags})
     b->release();
   for (int q = 0; q < 4; ++q)
@@ -203,6 +205,13 @@ extern "C" rt_status rt_set_launch(rt_handle* h, int32_t grid_ctas, int64_t tree
   return RT_OK;
 }
 
+extern "C" rt_status rt_set_pool(rt_handle* h, int32_t pool_entries) {
+  if (!h) return fail(RT_E_ARG, "null handle");
+  if (pool_entries < 0) return fail(RT_E_ARG, "negative pool size");
+  h->pool_override = pool_entries;
+  return RT_OK;
+}
+
 // ---------------------------------------------------------------------------
 // tree-walk launch (rows a3–a7)
 using KernelFn = void (*)(WalkParams);
@@ -214,11 +223,11 @@ static KernelFn pick_kernel() {
 
 // The kernel for (dim, g, rec) and the production (rec = false) kernel whose
 // occupancy fixes the launch geometry for both.
-static KernelFn kernel_for(int dim, int gk, bool rec, KernelFn* prod, int* smem, int* levels) {
+static KernelFn kernel_for(int dim, int gk, bool rec, KernelFn* prod, int* smem, int* pool_cap) {
 #define RT_K(D, G)                                                              \
   if (dim == D && gk == G) {                                                    \
     *smem = rtk::smem_bytes<D>();                                               \
-    *levels = rtk::Levels<D>::v;                                                \
+    *pool_cap = rtk::PoolCap<D>::v;                                             \
     *prod = pick_kernel<D, G, false>();                                         \
     return rec ? pick_kernel<D, G, true>() : pick_kernel<D, G, false>();        \
   }
@@ -244,14 +253,18 @@ static rt_status plan_launch(rt_handle* h, KernelFn fn, int smem, int64_t n_poin
   if (per_sm < 1) return fail(RT_E_CUDA, "tree_walk kernel cannot be resident");
   int grid = nsm * per_sm;
   if (h->grid_override > 0) grid = h->grid_override;
-  const int64_t warps = static_cast<int64_t>(grid) * rtk::kWarpsPerCta;
   const int64_t total = n_points * n_trees;
   int64_t T = h->tpt_override;
   if (T <= 0) {
-    // >= ~32 tasks per warp keeps the static round-robin balanced to ~3 %
-    T = total / (warps * 32);
-    T = std::max<int64_t>(T, 512);
-    T = std::min<int64_t>(T, 65536);
+    // Warps fetch tasks dynamically and run each from a clean start, so a
+    // task's sums depend on T alone; T is a function of the workload only
+    // (not of the grid) so results are bitwise identical on any GPU size.
+    // ~16 tasks per warp of a 4096-warp grid bound the end-of-launch tail;
+    // >= 1024 trees keep the per-task drain (idle lanes while a task's last
+    // trees finish) to a few percent; <= 16384 keeps tails short.
+    T = total / (int64_t(4096) * 16);
+    T = std::max<int64_t>(T, 1024);
+    T = std::min<int64_t>(T, 16384);
   }
   T = std::min<int64_t>(T, n_trees);
   // task ids are 32-bit in the kernel: grow tasks until they number < 2^31
@@ -347,9 +360,9 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
                           rtk::TreeRec* d_recs, double* d_sums, cudaStream_t st) {
   const rt_eq_params& p = h->p;
   const Norm& nz = h->nz;
-  int smem = 0, levels = 0;
+  int smem = 0, pool_cap = 0;
   KernelFn prod = nullptr;
-  KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, &prod, &smem, &levels);
+  KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, &prod, &smem, &pool_cap);
   if (!fn) return fail(RT_E_ARG, "no kernel for dim=%d init_kind=%d", p.dim, p.init_kind);
   if (smem > 48 * 1024) {
     RT_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -361,11 +374,14 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   const int nb = p.K + 2;
   const int nf = p.dim + 2;
   RT_CUDA(h->partials.ensure(static_cast<size_t>(L.n_tasks) * nb * 3 * sizeof(double)));
-  // stack levels beyond the shared-memory ones: [warps][K - LV][nf][32] doubles
-  const int spill_levels = std::max(0, p.K - levels);
-  const size_t spill_bytes = static_cast<size_t>(L.grid) * rtk::kWarpsPerCta * spill_levels *
-                             nf * 32 * sizeof(double);
-  RT_CUDA(h->spill.ensure(std::max<size_t>(spill_bytes, 256)));
+  // overflow stack entries once a warp's shared-memory pool is exhausted: a
+  // lane's stack never exceeds K groups, so 32 (K+1) entries per warp always
+  // suffice: [warps][gcap][nf] doubles and [warps][2][gcap] int32
+  const int gcap = 32 * (p.K + 1);
+  const size_t nwarps = static_cast<size_t>(L.grid) * rtk::kWarpsPerCta;
+  RT_CUDA(h->gpool.ensure(nwarps * gcap * nf * sizeof(double)));
+  RT_CUDA(h->gaux.ensure(nwarps * 2 * gcap * sizeof(int32_t)));
+  if (h->pool_override > 0) pool_cap = std::min(pool_cap, static_cast<int>(h->pool_override));
 
   WalkParams P;
   std::memset(&P, 0, sizeof(P));
@@ -393,17 +409,36 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   P.tpn = static_cast<int32_t>(L.tpn);
   P.n_tasks = static_cast<int32_t>(L.n_tasks);
   P.partials = static_cast<double*>(h->partials.p);
-  P.spill = static_cast<double*>(h->spill.p);
-  P.spill_levels = spill_levels;
+  P.pool_cap = pool_cap;
+  P.gpool = static_cast<double*>(h->gpool.p);
+  P.gaux = static_cast<int32_t*>(h->gaux.p);
+  P.gcap = gcap;
   P.recs = d_recs;
   P.rec_shift = rec_shift;
   P.n_rec = (n_trees + (int64_t(1) << rec_shift) - 1) >> rec_shift;
   P.stats = static_cast<unsigned long long*>(h->stats.p);
+  P.task_ctr = reinterpret_cast<unsigned int*>(P.stats + 5);
 
-  RT_CUDA(cudaMemsetAsync(h->stats.p, 0, 5 * sizeof(unsigned long long), st));
+  // debug: RT_WARP_TIMES=<file> appends one line per launch with every warp's
+  // start/end %globaltimer (load-balance diagnostics; never set in production)
+  const char* wt_path = std::getenv("RT_WARP_TIMES");
+  if (wt_path != nullptr) {
+    RT_CUDA(h->wtime.ensure(nwarps * 4 * sizeof(unsigned long long)));
+    P.wtime = static_cast<unsigned long long*>(h->wtime.p);
+  }
+  RT_CUDA(cudaMemsetAsync(h->stats.p, 0, 6 * sizeof(unsigned long long), st));   // + task counter
   RT_CUDA(cudaEventRecord(h->ev[0], st));
   fn<<<L.grid, rtk::kThreads, smem, st>>>(P);
   RT_CUDA(cudaGetLastError());
+  if (wt_path != nullptr) {
+    std::vector<unsigned long long> wt(nwarps * 4);
+    RT_CUDA(cudaMemcpyAsync(wt.data(), P.wtime, wt.size() * 8, cudaMemcpyDeviceToHost, st));
+    RT_CUDA(cudaStreamSynchronize(st));
+    if (FILE* f = std::fopen(wt_path, "a")) {
+      for (size_t q = 0; q < wt.size(); ++q) std::fprintf(f, "%llu%c", wt[q], q + 1 < wt.size() ? ' ' : '\n');
+      std::fclose(f);
+    }
+  }
   RT_CUDA(cudaEventRecord(h->ev[1], st));
   reduce_tasks_kernel<<<static_cast<unsigned>(n_points), 32, 0, st>>>(
       static_cast<double*>(h->partials.p), L.tpn, nb, d_sums,

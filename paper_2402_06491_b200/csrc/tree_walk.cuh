@@ -1,31 +1,37 @@
 // tree_walk.cuh — the random-tree walk kernel (rows a3–a7).
 //
-// One lane = one tree at a time; one warp = a static stream of (node, tree)
-// tasks.  Each loop iteration advances EVERY lane by exactly one particle, so
-// the expensive part of an iteration (2–3 Philox blocks, logs, Box–Muller,
+// One lane = one tree at a time; one warp = a dynamic stream of tasks (T
+// consecutive trees of one node, fetched with one atomicAdd each).  Each loop iteration advances EVERY lane by exactly one particle, so
+// the expensive part of an iteration (2 Philox blocks, logs, Box–Muller,
 // sqrt — PAPER.md:197-204 exponential clock, PAPER.md:174-191 Brownian
 // increment) runs with all 32 lanes converged whatever the trees look like;
 // the tree logic after it is short predicated straight-line code.  A lane
-// whose tree ends takes the next tree of the warp's stream in the next
-// iteration (ballot + popc compaction), so no lane idles until the stream
-// runs dry.
+// whose tree ends takes the next tree of the warp's stream in the same
+// iteration (ballot + popc rank), so no lane idles until the stream runs dry.
 //
-// Depth-first order (child 0 first): the pending sibling
-// groups form a per-lane stack in shared memory (SoA [level][field][lane],
-// conflict-free), with levels >= LV in a per-warp global spill area (rare:
-// LV is sized from the depth distribution).  A group stores the
-// split position y, remaining horizon τ_c and a packed (next child label |
-// remaining count << 56).
+// Depth-first order (child 0 first).  The pending sibling
+// groups of all 32 trees of a warp live in ONE per-warp pool of stack
+// entries in shared memory (SoA [field][entry]); each lane's stack is a
+// linked list through the entries' `prev` index, and entries are handed out
+// and returned through a per-warp free list with ballot ranks.  A per-lane
+// fixed-depth stack must be sized for each lane's deepest excursion; the
+// pool only for the warp's SUM of depths, which is far more concentrated
+// (cfg4: mean 58, p99.99 89 entries for 32 lanes, where per-lane stacks of 5
+// levels overflowed in 29 % of iterations — DESIGN.md §4).  Should the pool
+// run dry, further entries come from a per-warp area in global memory (slow
+// path, warp-uniform branch; exercised by the tests through rt_set_pool).
+// A group stores the split position y, remaining horizon τ_c and a packed
+// (next child label | remaining count << 56).
 //
 // Order binning: a finished tree appends
-// (bin | task slot << 5, C) to a 64-entry per-warp ring in shared memory and
-// bumps its slot's integer bin count (shared atomic: exact in any order);
-// when 32 records are pending the warp "transposes" them: lane b owns order
-// bin b and accumulates, in ring order, the records whose bin is b (ΣC, ΣC²;
-// deterministic).  When all trees of a task are recorded, lane b writes the
-// task's bin b to partials[task][b] (atomic-free); a second kernel sums each
-// node's tasks in task order.  Two task slots let the stream run past a task
-// boundary while the previous task's last trees finish.
+// (bin, C) to a 64-entry per-warp ring in shared memory; when 32 records are
+// pending the warp "transposes" them: lane b owns order bin b and
+// accumulates, in ring order, the records whose bin is b (ΣC, ΣC², count).
+// When all trees of a task are recorded, lane b writes the task's bin b to
+// partials[task][b] (atomic-free); a second kernel sums each node's tasks in
+// task order.  Each task runs from a clean start (all lanes begin it
+// together), so its partials depend on the task alone: results are bitwise
+// reproducible for a fixed task size, whatever the grid or warp timing.
 #pragma once
 #include <cstdint>
 
@@ -38,20 +44,18 @@ constexpr int kWarpsPerCta = 4;
 constexpr int kThreads = 32 * kWarpsPerCta;
 constexpr int kRing = 64;
 constexpr uint64_t kLabelMask = (1ull << 56) - 1;
-// per-warp record ring [kRing] (C, bin | slot << 5), bin sums [2 slots][2][32],
-// counts [2][32]; the ring is flushed completely once >= 32 records are pending
-constexpr int kWarpExtra = kRing * 8 + 2 * 2 * 32 * 8 + kRing * 4 + 2 * 32 * 4;
 
-// Stack levels kept in shared memory per lane, and resident CTAs per SM (the
-// register budget 65536 / (128 v) and the 228 KB of shared memory).  The
+// Stack-pool entries per warp in shared memory (<= 255: 8-bit free list) and
+// resident CTAs per SM.  Sized from the warp's depth-sum distribution (see
+// the header) and the 228 KB of shared memory / 64 K registers per SM.  The
 // record-emitting trace variant gets one CTA less so it never spills; it is
 // launched on the production kernel's grid, so both give identical sums.
-template <int DIM> struct Levels;
-template <> struct Levels<1> { static constexpr int v = 7; };
-template <> struct Levels<2> { static constexpr int v = 5; };
-template <> struct Levels<3> { static constexpr int v = 5; };
+template <int DIM> struct PoolCap;
+template <> struct PoolCap<1> { static constexpr int v = 144; };
+template <> struct PoolCap<2> { static constexpr int v = 136; };
+template <> struct PoolCap<3> { static constexpr int v = 112; };
 template <int DIM, bool REC> struct MinCtas {
-  static constexpr int v = (DIM == 3 ? 6 : 7) - (REC ? 1 : 0);
+  static constexpr int v = (DIM == 1 ? 8 : 7) - (REC ? 1 : 0);
 };
 
 struct TreeRec {   // mirrors rt_tree_rec
@@ -69,13 +73,29 @@ struct WalkParams {
   const double* points;
   int32_t n_trees, T, tpn, n_tasks;   // trees per node (< 2^31), per task, tasks per node, tasks
   uint32_t tree_offset;               // first tree index (tree indices are uint32)
+  int32_t pool_cap;                   // shared-memory pool entries used (<= PoolCap)
   double* partials;     // [n_tasks][nb][3]
-  double* spill;        // [warps][spill_levels][DIM+2][32]
-  int32_t spill_levels;
+  double* gpool;        // [warps][gcap][DIM+2]  overflow stack entries
+  int32_t* gaux;        // [warps][2][gcap]      overflow prev links, free list
+  int32_t gcap;         // overflow entries per warp (32 (K+1): every stack bound)
   TreeRec* recs;
   int32_t rec_shift;
   int64_t n_rec;
   unsigned long long* stats;   // trees, pruned, particles, leaves, splits
+  unsigned int* task_ctr;      // dynamic task counter (zeroed before the launch)
+  unsigned long long* wtime;   // debug (RT_WARP_TIMES): [warps][4] start, end, smid, iterations; or null
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Per-warp bookkeeping that only the completion path touches.
+struct WarpState {
+  double iss_y[3];          // coordinates of the current task's node
+  int gtop, gfree;          // overflow area: bump pointer, free-list size
 };
 
 template <int DIM, int GK>
@@ -93,14 +113,18 @@ __device__ __forceinline__ double g_eval(const double (&x)[DIM], const WalkParam
   }
 }
 
+// per-warp shared memory: pool fields [DIM+2][cap] doubles, ring (C, code)
+// [kRing], bin sums [ΣC, ΣC²][32] + counts [32], state, prev [cap] int16,
+// free list [cap] u8
 template <int DIM>
-__host__ __device__ constexpr int stack_bytes_per_warp() {
-  return Levels<DIM>::v * (DIM + 2) * 32 * 8;
+__host__ __device__ constexpr int warp_smem_bytes() {
+  return PoolCap<DIM>::v * ((DIM + 2) * 8 + 2 + 1) + kRing * 12 + 2 * 32 * 8 + 32 * 4 +
+         static_cast<int>(sizeof(WarpState));
 }
 
 template <int DIM>
 __host__ __device__ constexpr int smem_bytes() {
-  return 128 * 16 /* log table */ + kWarpsPerCta * (stack_bytes_per_warp<DIM>() + kWarpExtra) +
+  return 128 * 16 /* log table */ + kWarpsPerCta * ((warp_smem_bytes<DIM>() + 15) / 16 * 16) +
          9 * 8 + 9 * 4 /* offspring weights and sizes */;
 }
 
@@ -109,114 +133,181 @@ __global__ void __launch_bounds__(kThreads, MinCtas<DIM, REC>::v)
 tree_walk_kernel(const __grid_constant__ WalkParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int NF = DIM + 2;
-  constexpr int LV = Levels<DIM>::v;
+  constexpr int CAP = PoolCap<DIM>::v;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
 
   // ---- shared memory carve-up -------------------------------------------
   LogEntry* const ltab = reinterpret_cast<LogEntry*>(smem_raw);
-  unsigned char* const wbase = smem_raw + 128 * 16 + wib * (stack_bytes_per_warp<DIM>() + kWarpExtra);
-  double* const ssp = reinterpret_cast<double*>(wbase) + lane;            // [LV][NF][32]
-  double* const ringC = reinterpret_cast<double*>(wbase + stack_bytes_per_warp<DIM>());
-  double* const bsum = ringC + kRing;                                     // [slot][ΣC, ΣC²][32]
-  int* const ringBin = reinterpret_cast<int*>(bsum + 2 * 2 * 32);         // [kRing]
-  int* const bcnt = ringBin + kRing;                                      // [slot][32]
+  unsigned char* const wbase = smem_raw + 128 * 16 + wib * ((warp_smem_bytes<DIM>() + 15) / 16 * 16);
+  double* const pool = reinterpret_cast<double*>(wbase);                   // [NF][CAP]
+  double* const ringC = pool + NF * CAP;                                    // [kRing]
+  double* const bsum = ringC + kRing;                                       // [ΣC, ΣC²][32]
+  int* const bcnt = reinterpret_cast<int*>(bsum + 2 * 32);                  // [32]
+  WarpState* const ws = reinterpret_cast<WarpState*>(bcnt + 32);
+  int* const ringCode = reinterpret_cast<int*>(ws + 1);                     // [kRing]
+  int16_t* const prevS = reinterpret_cast<int16_t*>(ringCode + kRing);      // [CAP]
+  uint8_t* const freeS = reinterpret_cast<uint8_t*>(prevS + CAP);           // [CAP]
   double* const wtab = reinterpret_cast<double*>(smem_raw + 128 * 16 +
-      kWarpsPerCta * (stack_bytes_per_warp<DIM>() + kWarpExtra));        // [9] weights
+      kWarpsPerCta * ((warp_smem_bytes<DIM>() + 15) / 16 * 16));           // [9] weights
   int* const ktab = reinterpret_cast<int*>(wtab + 9);                     // [9] offspring k
   for (int q = threadIdx.x; q < 128; q += kThreads) ltab[q] = kLogTable[q];
   if (threadIdx.x < 9) {
     wtab[threadIdx.x] = P.w[threadIdx.x];
     ktab[threadIdx.x] = P.kval[threadIdx.x];
   }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) bsum[q * 32 + lane] = 0.0;
+  const int cap = P.pool_cap;
+  for (int q = lane; q < cap; q += 32) freeS[q] = static_cast<uint8_t>(q);
+  bsum[lane] = 0.0;
+  bsum[32 + lane] = 0.0;
   bcnt[lane] = 0;
-  bcnt[32 + lane] = 0;
-  __syncthreads();
 
   const int gwarp = blockIdx.x * kWarpsPerCta + wib;
-  const int W = gridDim.x * kWarpsPerCta;
-  double* const gsp = P.spill + static_cast<int64_t>(gwarp) * P.spill_levels * NF * 32 + lane;
+  if (P.wtime != nullptr && lane == 0) P.wtime[4 * gwarp] = global_ns();
+  unsigned long long n_iter = 0;
+  double* const gpool = P.gpool + static_cast<int64_t>(gwarp) * P.gcap * NF;
+  int* const gprev = P.gaux + static_cast<int64_t>(gwarp) * 2 * P.gcap;
+  int* const gfl = gprev + P.gcap;
 
-  // ---- warp-uniform stream state (32-bit) ----------------------------------
-  // the task being issued: id, trees issued / in it, its first tree index and
-  // its node's coordinates
-  int iss_task = gwarp, iss_next = 0, iss_size = 0, iss_slot = 0;
-  uint32_t iss_j0 = 0u, iss_node = 0u;
-  double iss_y[DIM];
-  bool stream_end = iss_task >= P.n_tasks;
-  auto open_task = [&](int task) {
-    const int node = task / P.tpn;
-    const int q = task - node * P.tpn;
-    iss_size = min(P.T, P.n_trees - q * P.T);
+  // ---- warp-uniform stream state -------------------------------------------
+  // The warp fetches tasks dynamically (one atomicAdd per task) and runs each
+  // task from a clean start: all 32 lanes take the task's first trees
+  // together and the task is closed only when its last tree is recorded.  A
+  // task's processing — and so its partial sums — is then a function of the
+  // task alone, whichever warp runs it and whatever ran before (bitwise
+  // deterministic for a fixed task size T, any grid).  Dynamic fetching
+  // absorbs the warp scheduler's unequal issue rates.
+  uint32_t iss_next = 0u, iss_end = 0u, iss_node = 0u;
+  int task = -1, left = 0;             // current task, its trees not yet recorded
+  bool stream_end = false;
+  auto next_task = [&]() {             // all lanes, converged
+    int t = 0;
+    if (lane == 0) t = static_cast<int>(atomicAdd(P.task_ctr, 1u));
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= P.n_tasks) { stream_end = true; return; }
+    task = t;
+    const int node = t / P.tpn;
+    const int q = t - node * P.tpn;
+    const int size = min(P.T, P.n_trees - q * P.T);
     iss_node = static_cast<uint32_t>(node);
-    iss_j0 = static_cast<uint32_t>(P.tree_offset) + static_cast<uint32_t>(q * P.T);
+    iss_next = static_cast<uint32_t>(P.tree_offset) + static_cast<uint32_t>(q * P.T);
+    iss_end = iss_next + static_cast<uint32_t>(size);
+    left = size;
+    __syncwarp();
+    if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < DIM; ++k) iss_y[k] = P.points[node * DIM + k];
+      for (int k = 0; k < DIM; ++k) ws->iss_y[k] = P.points[static_cast<int64_t>(node) * DIM + k];
+    }
+    __syncwarp();
   };
-#pragma unroll
-  for (int k = 0; k < DIM; ++k) iss_y[k] = 0.0;
-  if (!stream_end) open_task(iss_task);
-  // per task slot: task id and trees not yet recorded (kFree: slot unused)
-  constexpr int kFree = -(1 << 30);
-  int slot_task0 = stream_end ? -1 : iss_task, slot_task1 = -1;
-  int slot_left0 = stream_end ? kFree : iss_size, slot_left1 = kFree;
   int ring_cnt = 0;    // pending records (always flushed completely)
-  int ring_mask = 0;   // bit s: some pending record belongs to task slot s
+  int nfree = cap;     // free shared-memory pool entries
+  int n_glob = 0;      // overflow entries in use (warp-uniform)
 
   // ---- lane state ----------------------------------------------------------
   bool active = false;
-  int slot = 0;
   uint32_t ti = 0, tj = 0;
   double y[DIM];
 #pragma unroll
   for (int k = 0; k < DIM; ++k) y[k] = 0.0;
   double tau = 0.0, Pi = 1.0;
   uint64_t label = 1;
-  int ne = 0, sp = 0;
+  int ne = 0, top = -1;                // top: the lane's top stack entry (-1: empty)
   int leaves = 0, parts = 0;           // per-tree counts (trace variant only)
   uint32_t c_part = 0u, c_leaf = 0u;   // particles / leaves since the last task close
 
-  // Hand the next trees of the warp's stream to idle lanes (warp-uniform).
-  // Lanes only become idle when trees finish, so this runs at start-up and
-  // after a tree-completion event.
-  auto assign = [&]() {
-    unsigned idle = __ballot_sync(0xffffffffu, !active);
-    while (idle != 0u && !stream_end) {
-      const int avail = iss_size - iss_next;
-      if (avail == 0) {
-        const int nt = iss_task + W;
-        if (nt >= P.n_tasks) { stream_end = true; break; }
-        const int ns = iss_slot ^ 1;
-        if ((ns == 0 ? slot_left0 : slot_left1) != kFree) break;   // previous task still open
-        iss_task = nt; iss_next = 0; iss_slot = ns;
-        open_task(nt);
-        if (ns == 0) { slot_task0 = nt; slot_left0 = iss_size; }
-        else { slot_task1 = nt; slot_left1 = iss_size; }
-        continue;
-      }
-      const int nidle = __popc(idle);
-      const int take = min(avail, nidle);
-      const int rank = __popc(idle & lt_mask);
-      if (!active && rank < take) {
-        ti = iss_node;
-        tj = iss_j0 + static_cast<uint32_t>(iss_next + rank);
-        slot = iss_slot;
+  auto start_tree = [&](uint32_t j) {  // a fresh tree j of the current task
+    ti = iss_node;
+    tj = j;
 #pragma unroll
-        for (int k = 0; k < DIM; ++k) y[k] = iss_y[k];
-        tau = P.t; label = 1; Pi = 1.0; ne = 0; sp = 0;
-        if constexpr (REC) { leaves = 0; parts = 0; }
-        active = true;
-      }
+    for (int k = 0; k < DIM; ++k) y[k] = ws->iss_y[k];
+    tau = P.t; label = 1; Pi = 1.0; ne = 0; top = -1;
+    if constexpr (REC) { leaves = 0; parts = 0; }
+    active = true;
+  };
+
+  // Transpose the pending records into the bin sums: lane b owns bin b and
+  // accumulates, in ring order, ΣC, ΣC², count of the records of bin b.
+  auto flush = [&]() {
+    __syncwarp();
+    double s1 = bsum[lane], s2 = bsum[32 + lane];
+    int nn = 0;
+    for (int r = 0; r < ring_cnt; ++r) {
+      const double C = ringC[r];
+      if (ringCode[r] == lane) { s1 += C; s2 = fma(C, C, s2); ++nn; }
+    }
+    ring_cnt = 0;
+    bsum[lane] = s1;
+    bsum[32 + lane] = s2;
+    bcnt[lane] += nn;
+    __syncwarp();
+  };
+
+  // All trees of the task are recorded: write its partials (lane b = bin b),
+  // fold the event counters, fetch the next task and start its first trees.
+  auto close_and_next = [&]() {
+    flush();
+    if (lane < P.nb) {
+      double* o = P.partials + (static_cast<int64_t>(task) * P.nb + lane) * 3;
+      o[0] = bsum[lane];
+      o[1] = bsum[32 + lane];
+      o[2] = static_cast<double>(bcnt[lane]);
+    }
+    bsum[lane] = 0.0;
+    bsum[32 + lane] = 0.0;
+    bcnt[lane] = 0;
+    unsigned long long v0 = c_part, v1 = c_leaf;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+      v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+    }
+    if (lane == 0) {
+      atomicAdd(P.stats + 2, v0);
+      atomicAdd(P.stats + 3, v1);
+    }
+    c_part = 0u;
+    c_leaf = 0u;
+    next_task();
+    if (!stream_end) {
+      const uint32_t take = min(iss_end - iss_next, 32u);
+      if (static_cast<uint32_t>(lane) < take) start_tree(iss_next + static_cast<uint32_t>(lane));
       iss_next += take;
-      idle = __ballot_sync(0xffffffffu, !active);
     }
   };
-  assign();
+
+  // ---- stack-pool slow path (overflow entries in global memory) -----------
+  // entry e < cap lives in shared memory, e >= cap at gpool[e - cap]
+  auto fld = [&](int e, int f) -> double* {
+    return e < cap ? pool + f * CAP + e : gpool + static_cast<int64_t>(e - cap) * NF + f;
+  };
+  auto prev_of = [&](int e) -> int { return e < cap ? static_cast<int>(prevS[e]) : gprev[e - cap]; };
+  // return entry e of every lane with rel set to the free lists
+  auto release_generic = [&](bool rel, int e) {
+    const unsigned rs = __ballot_sync(0xffffffffu, rel && e < cap);
+    const unsigned rg = __ballot_sync(0xffffffffu, rel && e >= cap);
+    const int gf = ws->gfree;
+    __syncwarp();
+    if (rel && e < cap) freeS[nfree + __popc(rs & lt_mask)] = static_cast<uint8_t>(e);
+    if (rel && e >= cap) gfl[gf + __popc(rg & lt_mask)] = e - cap;
+    nfree += __popc(rs);
+    n_glob -= __popc(rg);
+    if (lane == 0) ws->gfree = gf + __popc(rg);
+    __syncwarp();
+  };
+
+  if (lane == 0) ws->gtop = ws->gfree = 0;
+  __syncthreads();
+  next_task();
+  if (!stream_end) {
+    const uint32_t take = min(iss_end - iss_next, 32u);
+    if (static_cast<uint32_t>(lane) < take) start_tree(iss_next + static_cast<uint32_t>(lane));
+    iss_next += take;
+  }
 
   while (true) {
+    if (P.wtime != nullptr) ++n_iter;
     if (stream_end) {                                  // warp-uniform
       if (!__any_sync(0xffffffffu, active)) break;
     }
@@ -285,61 +376,96 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     }
     const bool push = branch && k > 1;           // k-1 younger siblings wait
     const bool pop = (active && leaf) || (branch && k == 0);
+    const bool has = pop && top >= 0;            // resume the top group's next child
+    const bool done = pruned || kill || (pop && top < 0);
     const double tc = tau - S;
     const uint64_t base = label << P.beta;
-    // push the younger siblings: shared-memory levels inline, the rare deep
-    // levels (global) behind a warp-uniform test so they cost nothing otherwise
     const uint64_t push_pk = (base | 1ull) | (static_cast<uint64_t>(k - 1) << 56);
-    if (push && sp < LV) {
-#pragma unroll
-      for (int q = 0; q < DIM; ++q) ssp[(sp * NF + q) * 32] = x[q];
-      ssp[(sp * NF + DIM) * 32] = tc;
-      ssp[(sp * NF + DIM + 1) * 32] = __longlong_as_double(static_cast<long long>(push_pk));
-    }
-    if (__any_sync(0xffffffffu, push && sp >= LV)) {
-      if (push && sp >= LV) {
-        double* b = gsp + (sp - LV) * (NF * 32);
-#pragma unroll
-        for (int q = 0; q < DIM; ++q) b[q * 32] = x[q];
-        b[DIM * 32] = tc;
-        b[(DIM + 1) * 32] = __longlong_as_double(static_cast<long long>(push_pk));
-      }
-    }
-    sp += push ? 1 : 0;
-    // continue with child 0 (lanes that pop overwrite this below; lanes whose
+    // continue with child 0 (popping lanes overwrite this below; lanes whose
     // tree ended are re-initialised at assignment)
 #pragma unroll
     for (int q = 0; q < DIM; ++q) y[q] = x[q];
     tau = tc;
     label = base;
-    const bool done = pruned || kill || (pop && sp == 0);
-    const int lvl = sp - 1;
-    const bool pop_s = pop && sp > 0 && lvl < LV;
-    uint64_t pk = 0;
-    if (pop_s) {
+
+    // ---------------- stack: pop / release / push ----------------------------
+    const unsigned alc = __ballot_sync(0xffffffffu, push);
+    const int nalc = __popc(alc);
+    if (n_glob == 0 && nalc <= nfree) {      // warp-uniform fast path
+      bool last = false;
+      if (has) {
 #pragma unroll
-      for (int q = 0; q < DIM; ++q) y[q] = ssp[(lvl * NF + q) * 32];
-      tau = ssp[(lvl * NF + DIM) * 32];
-      pk = static_cast<uint64_t>(__double_as_longlong(ssp[(lvl * NF + DIM + 1) * 32]));
-    }
-    if (__any_sync(0xffffffffu, pop && lvl >= LV)) {
-      if (pop && lvl >= LV) {
-        const double* b = gsp + (lvl - LV) * (NF * 32);
-#pragma unroll
-        for (int q = 0; q < DIM; ++q) y[q] = b[q * 32];
-        tau = b[DIM * 32];
-        pk = static_cast<uint64_t>(__double_as_longlong(b[(DIM + 1) * 32]));
-        if ((pk >> 56) != 1ull)
-          gsp[((lvl - LV) * NF + DIM + 1) * 32] =
-              __longlong_as_double(static_cast<long long>(pk + 1ull - (1ull << 56)));
+        for (int q = 0; q < DIM; ++q) y[q] = pool[q * CAP + top];
+        tau = pool[DIM * CAP + top];
+        const uint64_t pk = static_cast<uint64_t>(__double_as_longlong(pool[(DIM + 1) * CAP + top]));
+        label = pk & kLabelMask;
+        last = (pk >> 56) == 1ull;
+        if (!last)
+          pool[(DIM + 1) * CAP + top] = __longlong_as_double(static_cast<long long>(pk + 1ull - (1ull << 56)));
       }
-    }
-    if (pop && sp > 0) {
-      label = pk & kLabelMask;
-      if ((pk >> 56) == 1ull) sp = lvl;         // last sibling: drop the group
-      else if (lvl < LV)
-        ssp[(lvl * NF + DIM + 1) * 32] =
-            __longlong_as_double(static_cast<long long>(pk + 1ull - (1ull << 56)));
+      const bool rel = has && last;              // group exhausted: free its entry
+      const unsigned rl = __ballot_sync(0xffffffffu, rel);
+      if (rel) {
+        freeS[nfree + __popc(rl & lt_mask)] = static_cast<uint8_t>(top);
+        top = prevS[top];
+      }
+      nfree += __popc(rl);
+      __syncwarp();
+      if (push) {
+        const int e = freeS[nfree - 1 - __popc(alc & lt_mask)];
+#pragma unroll
+        for (int q = 0; q < DIM; ++q) pool[q * CAP + e] = x[q];
+        pool[DIM * CAP + e] = tc;
+        pool[(DIM + 1) * CAP + e] = __longlong_as_double(static_cast<long long>(push_pk));
+        prevS[e] = static_cast<int16_t>(top);
+        top = e;
+      }
+      nfree -= nalc;
+    } else {                                     // generic path (overflow in use)
+      bool last = false;
+      if (has) {
+#pragma unroll
+        for (int q = 0; q < DIM; ++q) y[q] = *fld(top, q);
+        tau = *fld(top, DIM);
+        double* const pkp = fld(top, DIM + 1);
+        const uint64_t pk = static_cast<uint64_t>(__double_as_longlong(*pkp));
+        label = pk & kLabelMask;
+        last = (pk >> 56) == 1ull;
+        if (!last) *pkp = __longlong_as_double(static_cast<long long>(pk + 1ull - (1ull << 56)));
+      }
+      const bool rel = has && last;
+      const int freed = top;
+      if (rel) top = prev_of(top);
+      release_generic(rel, freed);
+      // allocate: shared entries first, then overflow entries
+      const int rk = __popc(alc & lt_mask);
+      const int gf = ws->gfree, gt = ws->gtop;
+      __syncwarp();
+      if (push) {
+        int e;
+        if (rk < nfree) {
+          e = freeS[nfree - 1 - rk];
+        } else {
+          const int g = rk - nfree;             // g-th overflow entry of this round
+          e = cap + (g < gf ? gfl[gf - 1 - g] : gt + (g - gf));
+        }
+#pragma unroll
+        for (int q = 0; q < DIM; ++q) *fld(e, q) = x[q];
+        *fld(e, DIM) = tc;
+        *fld(e, DIM + 1) = __longlong_as_double(static_cast<long long>(push_pk));
+        if (e < cap) prevS[e] = static_cast<int16_t>(top);
+        else gprev[e - cap] = top;
+        top = e;
+      }
+      const int ng = max(0, nalc - nfree);
+      nfree = max(0, nfree - nalc);
+      if (lane == 0) {
+        const int from_list = min(ng, gf);
+        ws->gfree = gf - from_list;
+        ws->gtop = gt + (ng - from_list);
+      }
+      n_glob += ng;
+      __syncwarp();
     }
 
     if constexpr (REC) {
@@ -352,102 +478,49 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       }
     }
 
-    // ---------------- record finished trees; flush; close tasks -------------
+    // ---------------- record finished trees; assign new ones -----------------
     const unsigned fin = __ballot_sync(0xffffffffu, done);
     if (fin != 0u) {
-      const unsigned fin1 = __ballot_sync(0xffffffffu, done && slot == 1);
-      const unsigned fin0 = fin & ~fin1;
+      // a pruned tree aborts with groups still pending: return its entries
+      bool drain = done && top >= 0;
+      while (__any_sync(0xffffffffu, drain)) {
+        const int e = top;
+        if (drain) top = prev_of(top);
+        release_generic(drain, e);
+        drain = drain && top >= 0;
+      }
+      const int nfin = __popc(fin);
+      const int rank = __popc(fin & lt_mask);
       if (done) {
-        const int bin = pruned ? (P.K + 1) : ne;
-        const int e = ring_cnt + __popc(fin & lt_mask);
-        ringBin[e] = bin | (slot << 5);
-        ringC[e] = pruned ? 0.0 : Pi;
-        atomicAdd(bcnt + slot * 32 + bin, 1);   // integer: exact in any order
-        active = false;
+        ringCode[ring_cnt + rank] = pruned ? (P.K + 1) : ne;
+        ringC[ring_cnt + rank] = pruned ? 0.0 : Pi;
       }
-      const int n1 = __popc(fin1), n0 = __popc(fin) - n1;
-      ring_cnt += n0 + n1;
-      ring_mask |= (n1 ? 2 : 0) | (n0 ? 1 : 0);
-      slot_left0 -= n0;
-      slot_left1 -= n1;
-      __syncwarp();
-      const bool cl0 = slot_left0 == 0;
-      const bool cl1 = slot_left1 == 0;
-      if (cl0 || cl1 || ring_cnt >= 32) {
-        // transpose all pending records: lane b accumulates, in ring order, the
-        // records of bin b (one slot in the common case, both near task ends)
-        if (ring_mask != 3) {
-          const int sl = ring_mask >> 1;
-          double a1 = bsum[(sl * 2 + 0) * 32 + lane], a2 = bsum[(sl * 2 + 1) * 32 + lane];
-          const int code = lane | (sl << 5);
-          for (int r = 0; r < ring_cnt; ++r) {
-            const int b = ringBin[r];
-            const double C = ringC[r];
-            if (b == code) {
-              a1 += C;
-              a2 = fma(C, C, a2);
-            }
-          }
-          bsum[(sl * 2 + 0) * 32 + lane] = a1;
-          bsum[(sl * 2 + 1) * 32 + lane] = a2;
-        } else {
-          double a1 = bsum[lane], a2 = bsum[32 + lane];
-          double b1 = bsum[64 + lane], b2 = bsum[96 + lane];
-          for (int r = 0; r < ring_cnt; ++r) {
-            const int b = ringBin[r];
-            const double C = ringC[r];
-            if (b == lane) {
-              a1 += C;
-              a2 = fma(C, C, a2);
-            }
-            if (b == (lane | 32)) {
-              b1 += C;
-              b2 = fma(C, C, b2);
-            }
-          }
-          bsum[lane] = a1; bsum[32 + lane] = a2;
-          bsum[64 + lane] = b1; bsum[96 + lane] = b2;
-        }
-        ring_cnt = 0;
-        ring_mask = 0;
+      ring_cnt += nfin;
+      left -= nfin;
+      const uint32_t avail = iss_end - iss_next;
+      if (avail >= static_cast<uint32_t>(nfin)) {          // common: more trees of the task
         __syncwarp();
-      }
-#pragma unroll
-      for (int sl = 0; sl < 2; ++sl) {
-        const bool close = sl ? cl1 : cl0;
-        if (close) {
-          double a1 = bsum[(sl * 2 + 0) * 32 + lane], a2 = bsum[(sl * 2 + 1) * 32 + lane];
-          {
-            const int task = sl ? slot_task1 : slot_task0;
-            if (lane < P.nb) {
-              double* o = P.partials + (static_cast<int64_t>(task) * P.nb + lane) * 3;
-              o[0] = a1; o[1] = a2; o[2] = static_cast<double>(bcnt[sl * 32 + lane]);
-            }
-            bcnt[sl * 32 + lane] = 0;
-            a1 = 0.0; a2 = 0.0;
-            if (sl) { slot_task1 = -1; slot_left1 = kFree; }
-            else { slot_task0 = -1; slot_left0 = kFree; }
-            // fold the lanes' 32-bit event counters into the 64-bit totals
-            unsigned long long v0 = c_part, v1 = c_leaf;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              v0 += __shfl_xor_sync(0xffffffffu, v0, o);
-              v1 += __shfl_xor_sync(0xffffffffu, v1, o);
-            }
-            if (lane == 0) {
-              atomicAdd(P.stats + 2, v0);
-              atomicAdd(P.stats + 3, v1);
-            }
-            c_part = 0u;
-            c_leaf = 0u;
-          }
-          bsum[(sl * 2 + 0) * 32 + lane] = a1;
-          bsum[(sl * 2 + 1) * 32 + lane] = a2;
-          __syncwarp();
+        if (done) start_tree(iss_next + static_cast<uint32_t>(rank));
+        iss_next += static_cast<uint32_t>(nfin);
+      } else {                                             // the task's trees run out
+        __syncwarp();
+        if (done) {
+          if (static_cast<uint32_t>(rank) < avail) start_tree(iss_next + static_cast<uint32_t>(rank));
+          else active = false;
         }
+        iss_next += avail;
+        if (left == 0) close_and_next();                   // every tree recorded
       }
-      assign();                                // finished lanes take new trees
+      if (ring_cnt >= 32) flush();
     }
+  }
+  if (ring_cnt > 0) flush();
+  if (P.wtime != nullptr && lane == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    P.wtime[4 * gwarp + 1] = global_ns();
+    P.wtime[4 * gwarp + 2] = smid;
+    P.wtime[4 * gwarp + 3] = n_iter;
   }
   // (trees, pruned trees and splits follow exactly from the bin counts and are
   // added by the task-reduction kernel; every task close folded c_part/c_leaf)

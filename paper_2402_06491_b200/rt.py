@@ -24,7 +24,7 @@ PREC_FP64, PREC_FP32_POS = 0, 1
 # every symbol include/rt.h declares
 SYMBOLS = ("rt_create", "rt_destroy", "rt_estimate", "rt_estimate_dev", "rt_sums_dev",
            "rt_finalize_dev", "rt_pade", "rt_pade_dev", "rt_interface_values", "rt_trace_dev",
-           "rt_get_stats", "rt_set_launch", "rt_philox_dev", "rt_last_error")
+           "rt_get_stats", "rt_set_launch", "rt_set_pool", "rt_philox_dev", "rt_last_error")
 
 
 class RTError(RuntimeError):
@@ -80,6 +80,7 @@ def lib():
             "rt_trace_dev": ([H, dp, i64, C.c_double, i64, i64, u64, i32, vp, dp, vp]),
             "rt_get_stats": ([H, C.POINTER(Stats)]),
             "rt_set_launch": ([H, i32, i64]),
+            "rt_set_pool": ([H, i32]),
             "rt_philox_dev": ([u64, vp, i64, vp, vp]),
         }
         for name, args in sig.items():
@@ -161,6 +162,11 @@ class Estimator:
 
     def set_launch(self, grid_ctas: int = 0, trees_per_task: int = 0):
         _check(lib().rt_set_launch(self._h, grid_ctas, trees_per_task))
+
+    def set_pool(self, entries: int = 0):
+        """Cap the per-warp shared-memory stack pool (0 = automatic); smaller
+        pools push more stack entries to the global overflow area (tests)."""
+        _check(lib().rt_set_pool(self._h, entries))
 
     # -- device API ---------------------------------------------------------
     def estimate(self, points, t: float, n_trees: int, seed: int, stream=None):

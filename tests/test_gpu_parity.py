@@ -170,21 +170,42 @@ def test_offset_trace_matches_oracle(P, orc):
 
 
 def test_geometry_and_determinism(P):
-    """Bitwise run-to-run with a fixed geometry; other geometries differ only
-    in summation order (C identical per tree)."""
+    """Bitwise run-to-run; tasks run from a clean start, so for a fixed task
+    size the sums are bitwise identical on ANY grid; another task size changes
+    only the summation order (C identical per tree)."""
     eq, pts, t, _ = CASES["cfg2"]
     x = dev(pts)
     est = P.Estimator(eq)
     a = est.sums(x, t, 20_000, seed=1).cpu().numpy()
     b = est.sums(x, t, 20_000, seed=1).cpu().numpy()
     assert np.array_equal(a, b)
+    for grid in (7, 1, 333):
+        est.set_launch(grid_ctas=grid, trees_per_task=0)
+        c = est.sums(x, t, 20_000, seed=1).cpu().numpy()
+        assert np.array_equal(a, c), f"grid {grid} changed the sums"
     est.set_launch(grid_ctas=7, trees_per_task=333)
     c = est.sums(x, t, 20_000, seed=1).cpu().numpy()
     assert np.array_equal(a[:, :, 2], c[:, :, 2])
-    assert_nodes_close(c[:, :, 0], a[:, :, 0], rtol=1e-12, what="geometry")
+    assert_nodes_close(c[:, :, 0], a[:, :, 0], rtol=1e-12, what="task size")
     est.set_launch(grid_ctas=1, trees_per_task=20_000)
     d = est.sums(x, t, 20_000, seed=1).cpu().numpy()
     assert_nodes_close(d[:, :, 0], a[:, :, 0], rtol=1e-12, what="one CTA")
+
+
+@pytest.mark.parametrize("name,pool", [("cfg4", 1), ("cfg4", 9), ("cfg2_t2", 3), ("d3_gauss", 40)])
+def test_stack_pool_overflow(P, orc, name, pool):
+    """A small shared-memory stack pool pushes pending sibling groups to the
+    global overflow area; trees must still equal the oracle's, and the sums
+    must equal the default pool's bit for bit (the pool changes no order)."""
+    eq, pts, t, N = CASES[name]
+    x = dev(pts)
+    est = P.Estimator(eq)
+    ref_sums = est.sums(x, t, N, seed=99).cpu().numpy()
+    est.set_pool(pool)
+    rec, sums = est.trace(x, t, N, seed=99)
+    assert_trees_equal(rec, orc.trees(eq, pts, t, N, seed=99), eq["K"])
+    s_small = est.sums(x, t, N, seed=99).cpu().numpy()
+    assert np.array_equal(s_small, ref_sums), "pool size changed the sums"
 
 
 def test_host_api_equals_device_api(P):

@@ -8,6 +8,9 @@ tag=${1:-run}
 mkdir -p gpurun_out
 nproc > gpurun_out/host_$tag.txt; lscpu | grep -E 'Model name|^CPU\(s\)' >> gpurun_out/host_$tag.txt
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv >> gpurun_out/host_$tag.txt
+timeout 300 python __graft_entry__.py --smoke > gpurun_out/smoke_$tag.log 2>&1
+rc=$?; echo "smoke rc=$rc" >> gpurun_out/smoke_$tag.log
+if [ $rc -ne 0 ]; then echo "smoke failed"; tail -20 gpurun_out/smoke_$tag.log; exit 1; fi
 if [ "${2:-tests}" = "tests" ]; then
   timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 400 -rf -x > gpurun_out/gpu_tests_$tag.log 2>&1
   echo "tests rc=$?" >> gpurun_out/gpu_tests_$tag.log
@@ -26,3 +29,5 @@ if [ "${3:-full}" = "full" ]; then
         > gpurun_out/ncu_full_$tag.log 2>&1
 fi
 echo done
+RT_WARP_TIMES=gpurun_out/wt4_$tag.txt timeout 300 python tools/warp_times.py cfg4 1000000 > gpurun_out/wt_cfg4_$tag.log 2>&1
+rm -f gpurun_out/wt4_$tag.txt gpurun_out/wt4_$tag.txt.npy

@@ -18,8 +18,9 @@ ops = []
 for r in data:
     t = r[ix["Source"]].strip().split()
     ops.append((t[1] if t and t[0].startswith("@") else (t[0] if t else "")))
-# loop head = the YIELD instruction (one per iteration)
-it = next((c for c, o in zip(cnt, ops) if o.startswith("YIELD")), max(cnt))
+# one iteration = one particle step = the first Philox multiply (M0 = 0xD2511F53)
+src = [r[ix["Source"]] for r in data]
+it = next((c for c, t in zip(cnt, src) if "IMAD.WIDE.U32" in t and "-0x2daee0ad" in t and c > 0), max(cnt))
 print(f"iterations {it}, instructions/iteration {sum(cnt) / it:.1f}")
 cur, start = None, 0
 blocks = []
