@@ -66,7 +66,8 @@ typedef enum {
 
 typedef enum {
   RT_PREC_FP64 = 0,       /* everything FP64                                     */
-  RT_PREC_FP32_POS = 1    /* reserved: FP32 positions / FP64 accumulation (cfg5) */
+  RT_PREC_FP32_POS = 1    /* FP32 positions, increments and g; FP64 clock, weights,
+                             tree product and sums (cfg5 variant) */
 } rt_precision;
 
 typedef struct {
@@ -81,7 +82,7 @@ typedef struct {
   double  init_scale;   /* scale of g (> 0)                                        */
   int32_t K;            /* orders 0..K are kept; trees with Ne > K are pruned.     */
                         /* 0 <= K <= 30 and 1 + K*β <= 56 (β = child-digit bits)   */
-  int32_t precision;    /* rt_precision; only RT_PREC_FP64 is implemented          */
+  int32_t precision;    /* rt_precision                                            */
 } rt_eq_params;
 
 typedef struct {
@@ -119,7 +120,7 @@ typedef struct rt_handle rt_handle;
  * RT_E_ARG on: null pointers, dim ∉ {1,2,3}, D <= 0 or non-finite, degree ∉
  * [0,8], non-finite b/λ/amp/scale, scale <= 0, K ∉ [0,30], label width
  * 1 + K*β > 56, a support category of zero integer width, an unknown enum,
- * precision != RT_PREC_FP64.  An empty support (purely linear f) is legal. */
+ * an unknown precision.  An empty support (purely linear f) is legal. */
 rt_status rt_create(const rt_eq_params* params, rt_handle** out);
 
 /* Free the handle and its device scratch.  NULL is a no-op. */

@@ -162,8 +162,8 @@ extern "C" rt_status rt_create(const rt_eq_params* params, rt_handle** out) {
   if (!(p.init_scale > 0.0) || !is_fin(p.init_scale))
     return fail(RT_E_ARG, "init_scale must be finite and > 0");
   if (p.K < 0 || p.K > 30) return fail(RT_E_ARG, "K must be in [0, 30] (got %d)", p.K);
-  if (p.precision != RT_PREC_FP64)
-    return fail(RT_E_ARG, "precision %d is not implemented (only RT_PREC_FP64)", p.precision);
+  if (p.precision != RT_PREC_FP64 && p.precision != RT_PREC_FP32_POS)
+    return fail(RT_E_ARG, "unknown precision %d", p.precision);
   Norm nz;
   rt_status s = normalize(p, nz);
   if (s != RT_OK) return s;
@@ -216,20 +216,25 @@ extern "C" rt_status rt_set_pool(rt_handle* h, int32_t pool_entries) {
 // tree-walk launch (rows a3–a7)
 using KernelFn = void (*)(WalkParams);
 
-template <int DIM, int GK, bool REC>
+template <int DIM, int GK, bool REC, bool F32>
 static KernelFn pick_kernel() {
-  return rtk::tree_walk_kernel<DIM, GK, REC>;
+  return rtk::tree_walk_kernel<DIM, GK, REC, F32>;
 }
 
 // The kernel for (dim, g, rec) and the production (rec = false) kernel whose
 // occupancy fixes the launch geometry for both.
-static KernelFn kernel_for(int dim, int gk, bool rec, KernelFn* prod, int* smem, int* pool_cap) {
+static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, KernelFn* prod, int* smem,
+                           int* pool_cap) {
 #define RT_K(D, G)                                                              \
   if (dim == D && gk == G) {                                                    \
     *smem = rtk::smem_bytes<D>();                                               \
     *pool_cap = rtk::PoolCap<D>::v;                                             \
-    *prod = pick_kernel<D, G, false>();                                         \
-    return rec ? pick_kernel<D, G, true>() : pick_kernel<D, G, false>();        \
+    if (f32) {                                                                  \
+      *prod = pick_kernel<D, G, false, true>();                                 \
+      return rec ? pick_kernel<D, G, true, true>() : *prod;                     \
+    }                                                                           \
+    *prod = pick_kernel<D, G, false, false>();                                  \
+    return rec ? pick_kernel<D, G, true, false>() : *prod;                      \
   }
   RT_K(1, 0) RT_K(1, 1) RT_K(1, 2) RT_K(1, 3)
   RT_K(2, 0) RT_K(2, 1) RT_K(2, 2) RT_K(2, 3)
@@ -362,7 +367,8 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   const Norm& nz = h->nz;
   int smem = 0, pool_cap = 0;
   KernelFn prod = nullptr;
-  KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, &prod, &smem, &pool_cap);
+  KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, p.precision == RT_PREC_FP32_POS,
+                           &prod, &smem, &pool_cap);
   if (!fn) return fail(RT_E_ARG, "no kernel for dim=%d init_kind=%d", p.dim, p.init_kind);
   if (smem > 48 * 1024) {
     RT_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

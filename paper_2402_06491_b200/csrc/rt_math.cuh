@@ -149,11 +149,27 @@ RTM_HD void sincospi2(double a, double& s_out, double& c_out) {
   c_out = dfrom(dbits(co) ^ cneg);
 }
 
-// cos(pi a) only (a as in sincospi2).
+// cos(pi a) only, a ∈ [0, 2] on the 2^-52 grid: n = rint(a), f = a − n
+// exactly (|f| <= 1/2), cos(pi a) = (−1)^n cos(pi f) with one even polynomial
+// (no quadrant swap, half the work of sincospi2; absolute error < 1e-16).
 RTM_HD double cospi2(double a) {
-  double s, c;
-  sincospi2(a, s, c);
-  return c;
+  const double n = rint_d(a);
+  const double f = a - n;
+  const double f2 = f * f;
+  double p = kCosPiW[11];
+  p = fma_d(p, f2, kCosPiW[10]);
+  p = fma_d(p, f2, kCosPiW[9]);
+  p = fma_d(p, f2, kCosPiW[8]);
+  p = fma_d(p, f2, kCosPiW[7]);
+  p = fma_d(p, f2, kCosPiW[6]);
+  p = fma_d(p, f2, kCosPiW[5]);
+  p = fma_d(p, f2, kCosPiW[4]);
+  p = fma_d(p, f2, kCosPiW[3]);
+  p = fma_d(p, f2, kCosPiW[2]);
+  p = fma_d(p, f2, kCosPiW[1]);
+  p = fma_d(p, f2, kCosPiW[0]);
+  const uint64_t neg = (static_cast<uint64_t>(static_cast<int>(n)) & 1ull) << 63;
+  return dfrom(dbits(p) ^ neg);
 }
 
 // sqrt(a), a >= 0: rsqrt seed, one Newton step (2^-44), one Heron correction.

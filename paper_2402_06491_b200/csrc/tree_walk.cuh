@@ -34,6 +34,7 @@
 // reproducible for a fixed task size, whatever the grid or warp timing.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "philox.cuh"
 #include "rt_math.cuh"
@@ -42,7 +43,7 @@ namespace rtk {
 
 constexpr int kWarpsPerCta = 4;
 constexpr int kThreads = 32 * kWarpsPerCta;
-constexpr int kRing = 64;
+constexpr int kRing = 64;   // >= 31 pending + 32 new records, padded to 4
 constexpr uint64_t kLabelMask = (1ull << 56) - 1;
 
 // Stack-pool entries per warp in shared memory (<= 255: 8-bit free list) and
@@ -55,7 +56,7 @@ template <> struct PoolCap<1> { static constexpr int v = 144; };
 template <> struct PoolCap<2> { static constexpr int v = 136; };
 template <> struct PoolCap<3> { static constexpr int v = 112; };
 template <int DIM, bool REC> struct MinCtas {
-  static constexpr int v = (DIM == 1 ? 8 : 7) - (REC ? 1 : 0);
+  static constexpr int v = 8 - (REC ? 1 : 0);
 };
 
 struct TreeRec {   // mirrors rt_tree_rec
@@ -99,7 +100,7 @@ struct WarpState {
 };
 
 template <int DIM, int GK>
-__device__ __forceinline__ double g_eval(const double (&x)[DIM], const WalkParams& P) {
+__device__ __forceinline__ double g_eval(const double (&x)[DIM], const WalkParams& P) {   // g(x)
   if constexpr (GK == 0) {
     return P.amp;
   } else if constexpr (GK == 1) {
@@ -110,6 +111,25 @@ __device__ __forceinline__ double g_eval(const double (&x)[DIM], const WalkParam
     if constexpr (DIM >= 3) r2 = fma(x[2], x[2], r2);
     if constexpr (GK == 2) return P.amp * exp_neg(-r2 * P.inv_scale2);
     else return P.amp * rcp_nr(fma(r2, P.inv_scale2, 1.0));
+  }
+}
+
+// g in single precision for the FP32-position variant (RT_PREC_FP32_POS):
+// CUDA's accurate single-precision routines (expf, tanhf: a few ulp).
+template <int DIM, int GK>
+__device__ __forceinline__ float g_eval_f(const float (&x)[DIM], const WalkParams& P) {
+  const float amp = static_cast<float>(P.amp);
+  if constexpr (GK == 0) {
+    return amp;
+  } else if constexpr (GK == 1) {
+    return amp * 0.5f * (1.0f + tanhf(x[0] * static_cast<float>(P.inv_scale)));
+  } else {
+    float r2 = x[0] * x[0];
+    if constexpr (DIM >= 2) r2 = fmaf(x[1], x[1], r2);
+    if constexpr (DIM >= 3) r2 = fmaf(x[2], x[2], r2);
+    const float is2 = static_cast<float>(P.inv_scale2);
+    if constexpr (GK == 2) return amp * expf(-r2 * is2);
+    else return amp / fmaf(r2, is2, 1.0f);
   }
 }
 
@@ -128,9 +148,14 @@ __host__ __device__ constexpr int smem_bytes() {
          9 * 8 + 9 * 4 /* offspring weights and sizes */;
 }
 
-template <int DIM, int GK, bool REC>
+// F32 = the FP32-position / FP64-accumulate variant (cfg5, BASELINE.json
+// configs[4]): the clock S, the leaf test, horizons, weights, the tree
+// product and all sums stay FP64 (tree structure identical to the FP64
+// path); positions, the Brownian increment and g are single precision.
+template <int DIM, int GK, bool REC, bool F32>
 __global__ void __launch_bounds__(kThreads, MinCtas<DIM, REC>::v)
 tree_walk_kernel(const __grid_constant__ WalkParams P) {
+  using PT = typename std::conditional<F32, float, double>::type;   // position type
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int NF = DIM + 2;
   constexpr int CAP = PoolCap<DIM>::v;
@@ -165,7 +190,6 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 
   const int gwarp = blockIdx.x * kWarpsPerCta + wib;
   if (P.wtime != nullptr && lane == 0) P.wtime[4 * gwarp] = global_ns();
-  unsigned long long n_iter = 0;
   double* const gpool = P.gpool + static_cast<int64_t>(gwarp) * P.gcap * NF;
   int* const gprev = P.gaux + static_cast<int64_t>(gwarp) * 2 * P.gcap;
   int* const gfl = gprev + P.gcap;
@@ -208,9 +232,9 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   // ---- lane state ----------------------------------------------------------
   bool active = false;
   uint32_t ti = 0, tj = 0;
-  double y[DIM];
+  PT y[DIM];
 #pragma unroll
-  for (int k = 0; k < DIM; ++k) y[k] = 0.0;
+  for (int k = 0; k < DIM; ++k) y[k] = PT(0);
   double tau = 0.0, Pi = 1.0;
   uint64_t label = 1;
   int ne = 0, top = -1;                // top: the lane's top stack entry (-1: empty)
@@ -221,7 +245,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     ti = iss_node;
     tj = j;
 #pragma unroll
-    for (int k = 0; k < DIM; ++k) y[k] = ws->iss_y[k];
+    for (int k = 0; k < DIM; ++k) y[k] = static_cast<PT>(ws->iss_y[k]);
     tau = P.t; label = 1; Pi = 1.0; ne = 0; top = -1;
     if constexpr (REC) { leaves = 0; parts = 0; }
     active = true;
@@ -230,12 +254,21 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   // Transpose the pending records into the bin sums: lane b owns bin b and
   // accumulates, in ring order, ΣC, ΣC², count of the records of bin b.
   auto flush = [&]() {
+    // pad the ring to a multiple of 4 with a code no lane owns, then read 4
+    // records per step with 16-byte loads (codes int4, values 2 x double2)
+    const int padded = (ring_cnt + 3) & ~3;
+    if (ring_cnt + lane < padded) ringCode[ring_cnt + lane] = -1;
     __syncwarp();
     double s1 = bsum[lane], s2 = bsum[32 + lane];
     int nn = 0;
-    for (int r = 0; r < ring_cnt; ++r) {
-      const double C = ringC[r];
-      if (ringCode[r] == lane) { s1 += C; s2 = fma(C, C, s2); ++nn; }
+    for (int r = 0; r < padded; r += 4) {
+      const int4 cd = *reinterpret_cast<const int4*>(ringCode + r);
+      const double2 ca = *reinterpret_cast<const double2*>(ringC + r);
+      const double2 cb = *reinterpret_cast<const double2*>(ringC + r + 2);
+      if (cd.x == lane) { s1 += ca.x; s2 = fma(ca.x, ca.x, s2); ++nn; }
+      if (cd.y == lane) { s1 += ca.y; s2 = fma(ca.y, ca.y, s2); ++nn; }
+      if (cd.z == lane) { s1 += cb.x; s2 = fma(cb.x, cb.x, s2); ++nn; }
+      if (cd.w == lane) { s1 += cb.y; s2 = fma(cb.y, cb.y, s2); ++nn; }
     }
     ring_cnt = 0;
     bsum[lane] = s1;
@@ -307,7 +340,6 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   }
 
   while (true) {
-    if (P.wtime != nullptr) ++n_iter;
     if (stream_end) {                                  // warp-uniform
       if (!__any_sync(0xffffffffu, active)) break;
     }
@@ -322,15 +354,46 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const bool leaf = S > tau;                  // 1{S > t}
     const double h2d = (leaf ? tau : S) * P.two_d;   // variance 2D·h of the increment
     // Box–Muller with the lifetime folded into the radius (R8):
-    // σ sqrt(h) · sqrt(-2 log v1) · (cos, sin)(2π v2)
-    double x[DIM];
-    if constexpr (DIM <= 2) {
+    // y ← y + σ sqrt(h) · sqrt(-2 log v1) · (cos, sin)(2π v2), in place
+    if constexpr (F32) {
+      // the same draws and formula in single precision
+      const float hf = static_cast<float>(h2d);
+      const float v1 = static_cast<float>(unif53(r1.x, r1.y));
+      if constexpr (DIM <= 2) {
+        const float v2 = static_cast<float>(unif53(r1.z, r1.w));
+        const float rad = sqrtf(-2.0f * logf(v1) * hf);
+        if constexpr (DIM == 1) {
+          y[0] = fmaf(rad, cospif(2.0f * v2), y[0]);
+        } else {
+          float sn, cs;
+          sincospif(2.0f * v2, &sn, &cs);
+          y[0] = fmaf(rad, cs, y[0]);
+          y[1] = fmaf(rad, sn, y[1]);
+        }
+      } else {
+        const float v2 = static_cast<float>(unif32(r0.w));
+        const float v3 = static_cast<float>(unif53(r1.z, r1.w));
+        const uint32_t w4 = ((r0.x & 0xFFFu) << 20) | ((r1.x & 0xFFFu) << 8) | ((r1.z & 0xFFFu) >> 4);
+        const float v4 = static_cast<float>(unif32(w4));
+        const float rad = sqrtf(-2.0f * logf(v1) * hf);
+        float sn, cs;
+        sincospif(2.0f * v2, &sn, &cs);
+        y[0] = fmaf(rad, cs, y[0]);
+        y[1] = fmaf(rad, sn, y[1]);
+        y[2] = fmaf(sqrtf(-2.0f * logf(v3) * hf), cospif(2.0f * v4), y[2]);
+      }
+    } else
+    if constexpr (DIM == 1) {                   // the cosine normal only
+      const double v1 = unif53(r1.x, r1.y), v2 = unif53(r1.z, r1.w);
+      const double rad = sqrt_nr(-2.0 * log_tab(v1, ltab) * h2d);
+      y[0] = fma(rad, cospi2(2.0 * v2), y[0]);
+    } else if constexpr (DIM == 2) {
       const double v1 = unif53(r1.x, r1.y), v2 = unif53(r1.z, r1.w);
       const double rad = sqrt_nr(-2.0 * log_tab(v1, ltab) * h2d);
       double sn, cs;
       sincospi2(2.0 * v2, sn, cs);
-      x[0] = fma(rad, cs, y[0]);
-      if constexpr (DIM >= 2) x[1] = fma(rad, sn, y[1]);
+      y[0] = fma(rad, cs, y[0]);
+      y[1] = fma(rad, sn, y[1]);
     } else {
       // d = 3 from the same two blocks (R8): radii uniforms from
       // block-1 (w1:w0), (w3:w2); angles from 32-bit uniforms — block-0 w3 and
@@ -342,10 +405,10 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       const double rad = sqrt_nr(-2.0 * log_tab(v1, ltab) * h2d);
       double sn, cs;
       sincospi2(2.0 * v2, sn, cs);
-      x[0] = fma(rad, cs, y[0]);
-      x[1] = fma(rad, sn, y[1]);
+      y[0] = fma(rad, cs, y[0]);
+      y[1] = fma(rad, sn, y[1]);
       const double rad2 = sqrt_nr(-2.0 * log_tab(v3, ltab) * h2d);
-      x[2] = fma(rad2, cospi2(2.0 * v4), y[2]);
+      y[2] = fma(rad2, cospi2(2.0 * v4), y[2]);
     }
     // categorical offspring choice from the integer thresholds (R9)
     // (thresholds past the support are 0xffffffff, so the sum needs no bound)
@@ -355,7 +418,9 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 #pragma unroll
       for (int q = 4; q < 8; ++q) s += (c32 > P.thr[q]) ? 1 : 0;
     }
-    const double gv = g_eval<DIM, GK>(x, P);    // g at the leaf
+    double gv;                                  // g at the leaf
+    if constexpr (F32) gv = static_cast<double>(g_eval_f<DIM, GK>(y, P));
+    else gv = g_eval<DIM, GK>(y, P);
     const int k = ktab[s];
     const double wk = wtab[s];
 
@@ -378,24 +443,33 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const bool pop = (active && leaf) || (branch && k == 0);
     const bool has = pop && top >= 0;            // resume the top group's next child
     const bool done = pruned || kill || (pop && top < 0);
-    const double tc = tau - S;
+    // child 0 continues from the split point y with horizon τ − S (popping
+    // lanes overwrite y, τ, label below; finished lanes are re-initialised)
+    tau -= S;
     const uint64_t base = label << P.beta;
     const uint64_t push_pk = (base | 1ull) | (static_cast<uint64_t>(k - 1) << 56);
-    // continue with child 0 (popping lanes overwrite this below; lanes whose
-    // tree ended are re-initialised at assignment)
-#pragma unroll
-    for (int q = 0; q < DIM; ++q) y[q] = x[q];
-    tau = tc;
     label = base;
 
-    // ---------------- stack: pop / release / push ----------------------------
+    // ---------------- stack: push / pop / release -----------------------------
+    // pushes first (they read y before pops overwrite it); entries released in
+    // this iteration are reused from the next one
     const unsigned alc = __ballot_sync(0xffffffffu, push);
     const int nalc = __popc(alc);
-    if (n_glob == 0 && nalc <= nfree) {      // warp-uniform fast path
+    if (n_glob == 0 && nalc <= nfree) {          // warp-uniform fast path
+      if (push) {
+        const int e = freeS[nfree - 1 - __popc(alc & lt_mask)];
+#pragma unroll
+        for (int q = 0; q < DIM; ++q) pool[q * CAP + e] = static_cast<double>(y[q]);
+        pool[DIM * CAP + e] = tau;
+        pool[(DIM + 1) * CAP + e] = __longlong_as_double(static_cast<long long>(push_pk));
+        prevS[e] = static_cast<int16_t>(top);
+        top = e;
+      }
+      nfree -= nalc;
       bool last = false;
       if (has) {
 #pragma unroll
-        for (int q = 0; q < DIM; ++q) y[q] = pool[q * CAP + top];
+        for (int q = 0; q < DIM; ++q) y[q] = static_cast<PT>(pool[q * CAP + top]);
         tau = pool[DIM * CAP + top];
         const uint64_t pk = static_cast<uint64_t>(__double_as_longlong(pool[(DIM + 1) * CAP + top]));
         label = pk & kLabelMask;
@@ -405,38 +479,13 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       }
       const bool rel = has && last;              // group exhausted: free its entry
       const unsigned rl = __ballot_sync(0xffffffffu, rel);
+      __syncwarp();
       if (rel) {
         freeS[nfree + __popc(rl & lt_mask)] = static_cast<uint8_t>(top);
         top = prevS[top];
       }
       nfree += __popc(rl);
-      __syncwarp();
-      if (push) {
-        const int e = freeS[nfree - 1 - __popc(alc & lt_mask)];
-#pragma unroll
-        for (int q = 0; q < DIM; ++q) pool[q * CAP + e] = x[q];
-        pool[DIM * CAP + e] = tc;
-        pool[(DIM + 1) * CAP + e] = __longlong_as_double(static_cast<long long>(push_pk));
-        prevS[e] = static_cast<int16_t>(top);
-        top = e;
-      }
-      nfree -= nalc;
     } else {                                     // generic path (overflow in use)
-      bool last = false;
-      if (has) {
-#pragma unroll
-        for (int q = 0; q < DIM; ++q) y[q] = *fld(top, q);
-        tau = *fld(top, DIM);
-        double* const pkp = fld(top, DIM + 1);
-        const uint64_t pk = static_cast<uint64_t>(__double_as_longlong(*pkp));
-        label = pk & kLabelMask;
-        last = (pk >> 56) == 1ull;
-        if (!last) *pkp = __longlong_as_double(static_cast<long long>(pk + 1ull - (1ull << 56)));
-      }
-      const bool rel = has && last;
-      const int freed = top;
-      if (rel) top = prev_of(top);
-      release_generic(rel, freed);
       // allocate: shared entries first, then overflow entries
       const int rk = __popc(alc & lt_mask);
       const int gf = ws->gfree, gt = ws->gtop;
@@ -450,8 +499,8 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
           e = cap + (g < gf ? gfl[gf - 1 - g] : gt + (g - gf));
         }
 #pragma unroll
-        for (int q = 0; q < DIM; ++q) *fld(e, q) = x[q];
-        *fld(e, DIM) = tc;
+        for (int q = 0; q < DIM; ++q) *fld(e, q) = static_cast<double>(y[q]);
+        *fld(e, DIM) = tau;
         *fld(e, DIM + 1) = __longlong_as_double(static_cast<long long>(push_pk));
         if (e < cap) prevS[e] = static_cast<int16_t>(top);
         else gprev[e - cap] = top;
@@ -466,6 +515,21 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       }
       n_glob += ng;
       __syncwarp();
+      bool last = false;
+      if (has) {
+#pragma unroll
+        for (int q = 0; q < DIM; ++q) y[q] = static_cast<PT>(*fld(top, q));
+        tau = *fld(top, DIM);
+        double* const pkp = fld(top, DIM + 1);
+        const uint64_t pk = static_cast<uint64_t>(__double_as_longlong(*pkp));
+        label = pk & kLabelMask;
+        last = (pk >> 56) == 1ull;
+        if (!last) *pkp = __longlong_as_double(static_cast<long long>(pk + 1ull - (1ull << 56)));
+      }
+      const bool rel = has && last;
+      const int freed = top;
+      if (rel) top = prev_of(top);
+      release_generic(rel, freed);
     }
 
     if constexpr (REC) {
@@ -520,7 +584,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     P.wtime[4 * gwarp + 1] = global_ns();
     P.wtime[4 * gwarp + 2] = smid;
-    P.wtime[4 * gwarp + 3] = n_iter;
+    P.wtime[4 * gwarp + 3] = 0;   // (iteration count: not recorded)
   }
   // (trees, pruned trees and splits follow exactly from the bin counts and are
   // added by the task-reduction kernel; every task close folded c_part/c_leaf)

@@ -55,7 +55,7 @@ def _create(rtmod, **kw):
     (dict(D=float("nan")), "D must"), (dict(degree=9), "degree"),
     (dict(init_kind=7), "init_kind"), (dict(init_scale=0.0), "init_scale"),
     (dict(K=-1), "K must"), (dict(K=31), "K must"), (dict(offspring=5), "offspring"),
-    (dict(precision=1), "precision"), (dict(init_amp=float("inf")), "init_amp"),
+    (dict(precision=2), "precision"), (dict(init_amp=float("inf")), "init_amp"),
     (dict(K=28), "label width"),                       # β = 2 for k_max = 4: 1 + 28*2 > 56
     (dict(b=[0, -1, 1e-12, 1.0] + [0] * 5, degree=3), "zero integer"),
 ])

@@ -208,6 +208,38 @@ def test_stack_pool_overflow(P, orc, name, pool):
     assert np.array_equal(s_small, ref_sums), "pool size changed the sums"
 
 
+@pytest.mark.parametrize("name", ["cfg2", "cfg2_t2", "cfg1", "cfg3", "cfg4", "heat_d2_tanh", "d3_gauss"])
+def test_fp32_positions_variant(P, orc, name):
+    """RT_PREC_FP32_POS (cfg5's FP32-position / FP64-accumulate variant): the
+    clock, leaf test and weights stay FP64, so tree structure equals the FP64
+    oracle's bit for bit; positions, increments and g are FP32, so C carries
+    single-precision error.  Bound (FP32 variant): a position
+    accumulates <= ~K+1 FP32 roundings of |x| <= ~8 plus ~2 ulp per increment,
+    |dx| <~ 2e-5; |d ln g / dx| <= 2|x|/scale^2 (Gaussian) <= 16, <= 1
+    (Lorentzian), ~1 (tanh): per leaf <~ 3e-4, typically 1e-6.  Asserted: every
+    tree within 1e-2 relative (+1e-30 absolute), 99.9 % within 1e-4, and the
+    node coefficients within 1e-4 relative."""
+    eq, pts, t, N = CASES[name]
+    eq32 = dict(eq, precision=W.PREC_FP32_POS)
+    est = P.Estimator(eq32)
+    rec, sums = est.trace(dev(pts), t, N, seed=12345)
+    ref = orc.trees(eq, pts, t, N, seed=12345)
+    assert np.array_equal(rec["ne"], ref["ne"]) and np.array_equal(rec["pruned"], ref["pruned"])
+    keep = ref["pruned"] == 0
+    assert np.array_equal(rec["leaves"][keep], ref["leaves"][keep])
+    assert np.array_equal(rec["particles"][keep], ref["particles"][keep])
+    rel = np.abs(rec["C"] - ref["C"]) / np.maximum(np.abs(ref["C"]), 1e-30)
+    print(f"{name}: FP32 per-tree rel err max {rel.max():.3e} p99.9 {np.quantile(rel, 0.999):.3e} "
+          f"median {np.median(rel):.3e}")
+    assert rel.max() <= 1e-2 and np.quantile(rel, 0.999) <= 1e-4
+    s_ref, _ = orc.sums(eq, pts, t, N, seed=12345)
+    s32 = sums.cpu().numpy()
+    assert np.array_equal(s32[:, :, 2], s_ref[:, :, 2])
+    big = np.abs(s_ref[:, :, 0]) > 1e-300
+    r = np.abs(s32[:, :, 0] - s_ref[:, :, 0])[big] / np.abs(s_ref[:, :, 0])[big]
+    assert r.max() <= 1e-4, r.max()
+
+
 def test_host_api_equals_device_api(P):
     eq, pts, t, _ = CASES["cfg3"]
     est = P.Estimator(eq)

@@ -19,7 +19,7 @@ def m(tmp_path_factory):
     subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fPIC", "-shared",
                            os.path.join(HERE, "helpers", "math_host.cpp"), "-o", so])
     lib = C.CDLL(so)
-    for f in ("m_log", "m_sqrt", "m_rcp", "m_exp"):
+    for f in ("m_log", "m_sqrt", "m_rcp", "m_exp", "m_cospi2"):
         getattr(lib, f).argtypes = [C.c_void_p, C.c_long, C.c_void_p]
     lib.m_sincospi2.argtypes = [C.c_void_p, C.c_long, C.c_void_p, C.c_void_p]
     return lib
@@ -73,6 +73,23 @@ def test_sincospi2(m):
     assert (s[-9], c[-9]) == (0.0, 1.0) and (s[-7], c[-7]) == (1.0, 0.0)
     assert (s[-5], c[-5]) == (0.0, -1.0) and (s[-3], c[-3]) == (-1.0, 0.0)
     assert (s[-1], c[-1]) == (0.0, 1.0)
+
+
+def test_cospi2_single_polynomial(m):
+    """cos(pi a) for a = 2v, v a 32-bit or 53-bit uniform (the d = 3 angle),
+    absolute error < 2.5 ulp(1) against long double (one Horner polynomial on
+    |f| <= 1/2 cancels near the zeros a = 1/2, 3/2; the Box-Muller normal r cos
+    then carries <= 2e-15 absolute error, far inside the 1e-12 per-tree
+    bound), exact at the extrema a = 0, 1, 2."""
+    rng = np.random.default_rng(5)
+    w = rng.integers(0, 2 ** 32, size=200_000, dtype=np.uint64)
+    a = np.concatenate([2.0 * (2 * w + 1).astype(np.float64) * 2.0 ** -33, 2.0 * _u53(200_000, 6),
+                        [0.0, 0.5, 1.0, 1.5, 2.0, 0.25, 0.75, 1.25, 1.75, 2.0 ** -40, 2 - 2.0 ** -40]])
+    got = _call(m, "m_cospi2", a)
+    pi = np.longdouble("3.14159265358979323846264338327950288")
+    ref = np.cos(pi * a.astype(np.longdouble))
+    assert float(np.max(np.abs(got - ref))) < 2.5 * EPS
+    assert got[-11] == 1.0 and got[-9] == -1.0 and got[-7] == 1.0
 
 
 def test_sqrt_rcp(m):

@@ -30,4 +30,5 @@ if [ "${3:-full}" = "full" ]; then
 fi
 echo done
 RT_WARP_TIMES=gpurun_out/wt4_$tag.txt timeout 300 python tools/warp_times.py cfg4 1000000 > gpurun_out/wt_cfg4_$tag.log 2>&1
-rm -f gpurun_out/wt4_$tag.txt gpurun_out/wt4_$tag.txt.npy
+RT_WARP_TIMES=gpurun_out/wt2_$tag.txt timeout 300 python tools/warp_times.py cfg2 1000000 > gpurun_out/wt_cfg2_$tag.log 2>&1
+rm -f gpurun_out/wt4_$tag.txt gpurun_out/wt4_$tag.txt.npy gpurun_out/wt2_$tag.txt gpurun_out/wt2_$tag.txt.npy
