@@ -115,21 +115,22 @@ __device__ __forceinline__ double g_eval(const double (&x)[DIM], const WalkParam
 }
 
 // g in single precision for the FP32-position variant (RT_PREC_FP32_POS):
-// CUDA's accurate single-precision routines (expf, tanhf: a few ulp).
+// MUFU exp2 (__expf) and single-precision reciprocals.
 template <int DIM, int GK>
 __device__ __forceinline__ float g_eval_f(const float (&x)[DIM], const WalkParams& P) {
   const float amp = static_cast<float>(P.amp);
   if constexpr (GK == 0) {
     return amp;
   } else if constexpr (GK == 1) {
-    return amp * 0.5f * (1.0f + tanhf(x[0] * static_cast<float>(P.inv_scale)));
+    // 0.5 (1 + tanh z) = 1 / (1 + e^{-2z}): no cancellation for z << 0 in FP32
+    return amp * __frcp_rn(1.0f + __expf(-2.0f * x[0] * static_cast<float>(P.inv_scale)));
   } else {
     float r2 = x[0] * x[0];
     if constexpr (DIM >= 2) r2 = fmaf(x[1], x[1], r2);
     if constexpr (DIM >= 3) r2 = fmaf(x[2], x[2], r2);
     const float is2 = static_cast<float>(P.inv_scale2);
-    if constexpr (GK == 2) return amp * expf(-r2 * is2);
-    else return amp / fmaf(r2, is2, 1.0f);
+    if constexpr (GK == 2) return amp * __expf(-r2 * is2);
+    else return amp * __frcp_rn(fmaf(r2, is2, 1.0f));
   }
 }
 
@@ -356,31 +357,34 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     // Box–Muller with the lifetime folded into the radius (R8):
     // y ← y + σ sqrt(h) · sqrt(-2 log v1) · (cos, sin)(2π v2), in place
     if constexpr (F32) {
-      // the same draws and formula in single precision
+      // the same draws and formula in single precision, on the MUFU
+      // approximations (lg2, sin/cos at |x| <= π, rsqrt seeds: ~2^-21)
+      constexpr float k2Pi = 6.28318530717958648f, kPi = 3.14159265358979324f;
       const float hf = static_cast<float>(h2d);
       const float v1 = static_cast<float>(unif53(r1.x, r1.y));
       if constexpr (DIM <= 2) {
         const float v2 = static_cast<float>(unif53(r1.z, r1.w));
-        const float rad = sqrtf(-2.0f * logf(v1) * hf);
+        const float rad = __fsqrt_rn(-2.0f * __logf(v1) * hf);
+        // cos(2πv) = −cos(2πv − π), sin(2πv) = −sin(2πv − π), argument in [−π, π)
         if constexpr (DIM == 1) {
-          y[0] = fmaf(rad, cospif(2.0f * v2), y[0]);
+          y[0] = fmaf(-rad, __cosf(fmaf(k2Pi, v2, -kPi)), y[0]);
         } else {
           float sn, cs;
-          sincospif(2.0f * v2, &sn, &cs);
-          y[0] = fmaf(rad, cs, y[0]);
-          y[1] = fmaf(rad, sn, y[1]);
+          __sincosf(fmaf(k2Pi, v2, -kPi), &sn, &cs);
+          y[0] = fmaf(-rad, cs, y[0]);
+          y[1] = fmaf(-rad, sn, y[1]);
         }
       } else {
         const float v2 = static_cast<float>(unif32(r0.w));
         const float v3 = static_cast<float>(unif53(r1.z, r1.w));
         const uint32_t w4 = ((r0.x & 0xFFFu) << 20) | ((r1.x & 0xFFFu) << 8) | ((r1.z & 0xFFFu) >> 4);
         const float v4 = static_cast<float>(unif32(w4));
-        const float rad = sqrtf(-2.0f * logf(v1) * hf);
+        const float rad = __fsqrt_rn(-2.0f * __logf(v1) * hf);
         float sn, cs;
-        sincospif(2.0f * v2, &sn, &cs);
-        y[0] = fmaf(rad, cs, y[0]);
-        y[1] = fmaf(rad, sn, y[1]);
-        y[2] = fmaf(sqrtf(-2.0f * logf(v3) * hf), cospif(2.0f * v4), y[2]);
+        __sincosf(fmaf(k2Pi, v2, -kPi), &sn, &cs);
+        y[0] = fmaf(-rad, cs, y[0]);
+        y[1] = fmaf(-rad, sn, y[1]);
+        y[2] = fmaf(-__fsqrt_rn(-2.0f * __logf(v3) * hf), __cosf(fmaf(k2Pi, v4, -kPi)), y[2]);
       }
     } else
     if constexpr (DIM == 1) {                   // the cosine normal only
