@@ -33,14 +33,16 @@ class Params(C.Structure):
     _fields_ = [("dim", C.c_int32), ("D", C.c_double), ("degree", C.c_int32),
                 ("b", C.c_double * 9), ("lam", C.c_double), ("offspring", C.c_int32),
                 ("init_kind", C.c_int32), ("init_amp", C.c_double),
-                ("init_scale", C.c_double), ("K", C.c_int32), ("precision", C.c_int32)]
+                ("init_scale", C.c_double), ("K", C.c_int32), ("precision", C.c_int32),
+                ("strategy", C.c_int32), ("q", C.c_double), ("coef_kind", C.c_int32 * 9),
+                ("coef_axis", C.c_int32), ("coef_scale", C.c_double), ("coef_t0", C.c_double)]
 
 
 class Norm(C.Structure):
     _fields_ = [("lam", C.c_double), ("inv_lambda", C.c_double), ("sigma", C.c_double),
                 ("a", C.c_double * 9), ("n_support", C.c_int32), ("support", C.c_int32 * 9),
                 ("thresh", C.c_uint64 * 9), ("p_hat", C.c_double * 9), ("w", C.c_double * 9),
-                ("beta", C.c_int32)]
+                ("beta", C.c_int32), ("tq", C.c_uint64), ("q_hat", C.c_double)]
 
 
 class TreeRec(C.Structure):
@@ -96,6 +98,12 @@ def params(eq: dict) -> Params:
     p.lam = eq.get("lam", 0.0); p.offspring = eq.get("offspring", 0)
     p.init_kind = eq["init_kind"]; p.init_amp = eq["init_amp"]
     p.init_scale = eq["init_scale"]; p.K = eq["K"]; p.precision = eq.get("precision", 0)
+    p.strategy = eq.get("strategy", 0); p.q = eq.get("q", 0.5)
+    ck = eq.get("coef_kind", [0] * 9)
+    for k in range(9):
+        p.coef_kind[k] = ck[k]
+    p.coef_axis = eq.get("coef_axis", 0); p.coef_scale = eq.get("coef_scale", 1.0)
+    p.coef_t0 = eq.get("coef_t0", 0.1)
     return p
 
 
@@ -124,7 +132,7 @@ def normalize(eq: dict) -> dict:
     ns = n.n_support
     return dict(lam=n.lam, inv_lambda=n.inv_lambda, sigma=n.sigma, a=list(n.a),
                 support=list(n.support)[:ns], thresh=list(n.thresh)[:ns],
-                p_hat=list(n.p_hat)[:ns], w=list(n.w)[:ns], beta=n.beta)
+                p_hat=list(n.p_hat)[:ns], w=list(n.w)[:ns], beta=n.beta, tq=n.tq, q_hat=n.q_hat)
 
 
 def trees(eq: dict, points: np.ndarray, t: float, n_trees: int, seed: int,

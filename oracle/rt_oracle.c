@@ -73,14 +73,34 @@ static void draw(uint64_t seed, int64_t i, int64_t j, uint64_t label, uint32_t c
 int or_normalize(const or_params* p, or_norm* o) {
   memset(o, 0, sizeof(*o));
   if (p->degree < 0 || p->degree > 8) return 1;
+  if (p->strategy < 0 || p->strategy > 2) return 3;
   double lam = p->lambda;
-  if (!(lam > 0.0)) lam = (p->b[1] < 0.0) ? -p->b[1] : 1.0;
+  /* strategy 0: λ = -b_1 if b_1 < 0 else 1 (R3); Strategy A's shift
+   * u = v e^{t} uses rate 1 unless overridden            */
+  if (!(lam > 0.0)) lam = (p->strategy == 0 && p->b[1] < 0.0) ? -p->b[1] : 1.0;
   o->lambda = lam;
   o->inv_lambda = 1.0 / lam;
   o->sigma = sqrt(2.0 * p->D);  /* generator D Δ = ½σ² Δ  (R5) */
   for (int k = 0; k <= 8; ++k) {
     o->a[k] = (k <= p->degree) ? p->b[k] : 0.0;
-    if (k == 1) o->a[k] += lam;
+    /* only the potential form moves -λu out of f; the shift (Eq. totalduhamel)
+     * and Strategy B (Eq. totalduhamel_B) sample every term of f, the linear
+     * one as a one-child "split"                                            */
+    if (k == 1 && p->strategy == 0) o->a[k] += lam;
+    if (p->coef_kind[k] != 0 && p->coef_kind[k] != 1) return 4;
+  }
+  /* a variable coefficient cannot ride on the potential's k = 1 term */
+  if (p->strategy == 0 && p->coef_kind[1] != 0) return 4;
+  for (int k = 0; k <= 8; ++k)
+    if (p->coef_kind[k] == 1 && !(p->coef_scale > 0.0 && p->coef_t0 > 0.0 &&
+                                  p->coef_axis >= 0 && p->coef_axis < p->dim)) return 4;
+  if (p->strategy == 2) {
+    /* ξ = 0 (leaf) iff a 32-bit draw is below tq: q̂ = tq / 2^32 exactly */
+    if (!(p->q > 0.0 && p->q < 1.0)) return 5;
+    uint64_t tq = (uint64_t)nearbyint(p->q * 4294967296.0);
+    if (tq == 0 || tq >= 4294967296ull) return 5;
+    o->tq = tq;
+    o->q_hat = (double)tq / 4294967296.0;
   }
   int ns = 0, kmax = 0;
   for (int k = 0; k <= 8; ++k)
@@ -109,7 +129,12 @@ int or_normalize(const or_params* p, or_norm* o) {
     if (T <= prev) return 2;            /* zero-width category: infinite weight */
     o->thresh[s] = T;
     o->p_hat[s] = (double)(T - prev) / 4294967296.0;
-    o->w[s] = o->a[o->support[s]] / (lam * o->p_hat[s]);
+    /* c'_α = c_α / p_α; Strategy B's c̃ = c / (1 - q)
+     * replaces the clock's 1/λ                              */
+    if (p->strategy == 2)
+      o->w[s] = o->a[o->support[s]] / ((1.0 - o->q_hat) * o->p_hat[s]);
+    else
+      o->w[s] = o->a[o->support[s]] / (lam * o->p_hat[s]);
     prev = T;
   }
   return 0;
@@ -131,6 +156,16 @@ static double g_eval(const or_params* p, const double* x) {
   }
 }
 
+/* Spatio-temporal factor of a variable coefficient c_k(x, t) = b_k φ(x, t),
+ * φ = e^{-x_a²/s²} / (t + t0) (Example 5: e^{-x²}/(t+0.1)),
+ * evaluated at the split position and the time argument of the children's
+ * sub-problem, c_α(y, t - s) (PAPER.md:237 h^{(α)}; PAPER.md:326 for B).     */
+static double coef_factor(const or_params* p, int k, const double* y, double tc) {
+  if (p->coef_kind[k] == 0) return 1.0;
+  double xa = y[p->coef_axis];
+  return exp(-(xa * xa) / (p->coef_scale * p->coef_scale)) / (tc + p->coef_t0);
+}
+
 /* ------------------------------------------------------------------------ */
 /* One tree (the generation procedure; Eq. recursion
  * PAPER.md:224-239; Eq. rep_strategyB).                   */
@@ -148,21 +183,39 @@ typedef struct {
 static double particle(tree_ctx* c, const double* y, double tau, uint64_t label) {
   const or_params* p = c->p;
   const or_norm* nz = c->nz;
-  uint32_t r0[4], r1[4];
+  uint32_t r0[4], r1[4], r2[4];
   c->particles++;
   draw(c->seed, c->i, c->j, label, 0, r0);
   draw(c->seed, c->i, c->j, label, 1, r1);
+  const int strat_b = (p->strategy == 2);
 
-  /* exponential clock S with density λ e^{-λS} */
-  double S = -log(or_unif53(r0[0], r0[1])) * nz->inv_lambda;
+  /* The particle's fate.  Strategy A (both forms): exponential clock S with
+   * density λ e^{-λS}; leaf iff S > τ (1{S > t}).
+   * Strategy B: ξ with P(ξ = 0) = q decides
+   * leaf / split; a split happens after the uniform fraction S of the
+   * horizon, the children inherit τ(1 - S).                                */
+  int is_leaf;
+  double h, tc;
+  if (strat_b) {
+    is_leaf = (uint64_t)r0[3] < nz->tq;                /* ξ = 0 */
+    double Sf = or_unif53(r0[0], r0[1]);               /* S ~ U(0,1) */
+    h = is_leaf ? tau : tau * Sf;
+    tc = tau * (1.0 - Sf);
+  } else {
+    double S = -log(or_unif53(r0[0], r0[1])) * nz->inv_lambda;
+    is_leaf = S > tau;
+    h = is_leaf ? tau : S;
+    tc = tau - S;
+  }
 
   /* Brownian increment over the particle's lifetime (Eqs. green, SDE,
    * PAPER.md:174-191): textbook Box–Muller normals.  d <= 2: one pair from
    * block 1 (radius uniform w1:w0, angle uniform w3:w2).  d = 3 (DESIGN.md
-   * R8): two pairs from the same two blocks — radii from block-1 words
-   * (w1:w0) and (w3:w2), angles from 32-bit uniforms: block-0 word 3, and the
-   * word assembled from the 12 low bits the 53-bit uniforms leave unused
-   * (block-0 w0, block-1 w0, block-1 w2).                               */
+   * R8): two pairs — radii from block-1 words (w1:w0) and (w3:w2); angles
+   * from 32-bit uniforms: Strategy A uses block-0 word 3 and the word
+   * assembled from the 12 low bits the 53-bit uniforms leave unused (block-0
+   * w0, block-1 w0, block-1 w2); Strategy B, whose block-0 word 3 is ξ, takes
+   * both angles from block 2 (words 0 and 1).                             */
   double xi[3];
   if (p->dim <= 2) {
     double v1 = or_unif53(r1[0], r1[1]), v2 = or_unif53(r1[2], r1[3]);
@@ -170,25 +223,32 @@ static double particle(tree_ctx* c, const double* y, double tau, uint64_t label)
     xi[0] = rr * cos(2.0 * M_PI * v2);
     xi[1] = rr * sin(2.0 * M_PI * v2);
   } else {
-    double v1 = or_unif53(r1[0], r1[1]), v2 = or_unif32(r0[3]);
-    double v3 = or_unif53(r1[2], r1[3]);
-    uint32_t w4 = ((r0[0] & 0xFFFu) << 20) | ((r1[0] & 0xFFFu) << 8) | ((r1[2] & 0xFFFu) >> 4);
-    double v4 = or_unif32(w4);
+    double v1 = or_unif53(r1[0], r1[1]), v3 = or_unif53(r1[2], r1[3]);
+    double v2, v4;
+    if (strat_b) {
+      draw(c->seed, c->i, c->j, label, 2, r2);
+      v2 = or_unif32(r2[0]);
+      v4 = or_unif32(r2[1]);
+    } else {
+      uint32_t w4 = ((r0[0] & 0xFFFu) << 20) | ((r1[0] & 0xFFFu) << 8) | ((r1[2] & 0xFFFu) >> 4);
+      v2 = or_unif32(r0[3]);
+      v4 = or_unif32(w4);
+    }
     double rr = sqrt(-2.0 * log(v1));
     xi[0] = rr * cos(2.0 * M_PI * v2);
     xi[1] = rr * sin(2.0 * M_PI * v2);
     xi[2] = sqrt(-2.0 * log(v3)) * cos(2.0 * M_PI * v4);
   }
-  double h = (S > tau) ? tau : S;
   double step = nz->sigma * sqrt(h);
   double x[3];
   for (int k = 0; k < p->dim; ++k) x[k] = y[k] + step * xi[k];
 
-  if (S > tau) {                       /* 1{S > t}: branch reaches the horizon */
+  if (is_leaf) {                       /* the branch reaches the horizon */
     c->leaves++;
-    return g_eval(p, x);               /* g at the leaf */
+    double gv = g_eval(p, x);          /* g at the leaf */
+    return strat_b ? gv / nz->q_hat : gv;   /* g̃ = g / q */
   }
-  /* 1{S <= t}: splitting event */
+  /* splitting event */
   c->ne++;
   if (c->ne > p->K) { c->stop = 1; return 0.0; }   /* prune */
   if (nz->n_support == 0) { c->stop = 2; return 0.0; }
@@ -196,13 +256,24 @@ static double particle(tree_ctx* c, const double* y, double tau, uint64_t label)
   int s = 0;
   while (!((uint64_t)u < nz->thresh[s])) ++s;
   int k = nz->support[s];
-  double val = nz->w[s];               /* h^(α) = c'_α */
+  /* h^(α)(y, s) = c'_α(y, t - s) e^{(t-s)(α-1)} (the factor
+   * e^{(α-1)τ_c} only with the shift, the child horizon τ_c = t - s, DESIGN.md
+   * reading C18); Strategy B: η(τ) c̃'_α(y, τ(1 - S)) with η(τ) = τ
+   *                                                      */
+  double val = nz->w[s] * coef_factor(p, k, x, tc);
+  if (p->strategy == 1) val *= exp((double)(k - 1) * nz->lambda * tc);
+  if (strat_b) val *= tau;
   for (int ch = 0; ch < k; ++ch) {
     uint64_t child = (label << nz->beta) | (uint64_t)ch;
-    val *= particle(c, x, tau - S, child);
+    val *= particle(c, x, tc, child);
     if (c->stop) return 0.0;
   }
   return val;
+}
+
+/* Root factor: Strategy A's shift estimates v, and u = v e^{λt}. */
+static double root_factor(const or_params* p, const or_norm* nz, double t) {
+  return p->strategy == 1 ? exp(nz->lambda * t) : 1.0;
 }
 
 int or_tree(const or_params* p, const double* x, int64_t i, int64_t j, double t,
@@ -211,7 +282,7 @@ int or_tree(const or_params* p, const double* x, int64_t i, int64_t j, double t,
   int e = or_normalize(p, &nz);
   if (e) return e;
   tree_ctx c = {p, &nz, seed, i, j, 0, 0, 0, 0};
-  double C = particle(&c, x, t, 1u);
+  double C = root_factor(p, &nz, t) * particle(&c, x, t, 1u);
   rec->ne = c.ne;
   rec->leaves = c.leaves;
   rec->particles = c.particles;
@@ -228,7 +299,7 @@ int or_trees(const or_params* p, const double* points, int64_t n_points, double 
   for (int64_t i = 0; i < n_points; ++i)
     for (int64_t q = 0; q < n_trees; ++q) {
       tree_ctx c = {p, &nz, seed, i, j0 + q, 0, 0, 0, 0};
-      double C = particle(&c, points + i * p->dim, t, 1u);
+      double C = root_factor(p, &nz, t) * particle(&c, points + i * p->dim, t, 1u);
       or_tree_rec* r = rec + i * n_trees + q;
       r->ne = c.ne; r->leaves = c.leaves; r->particles = c.particles;
       r->pruned = (c.stop == 1);
@@ -247,7 +318,7 @@ int or_trees_at(const or_params* p, const double* points, int64_t n_points, doub
   for (int64_t i = 0; i < n_points; ++i)
     for (int64_t q = 0; q < n_js; ++q) {
       tree_ctx c = {p, &nz, seed, i, js[q], 0, 0, 0, 0};
-      double C = particle(&c, points + i * p->dim, t, 1u);
+      double C = root_factor(p, &nz, t) * particle(&c, points + i * p->dim, t, 1u);
       or_tree_rec* r = rec + i * n_js + q;
       r->ne = c.ne; r->leaves = c.leaves; r->particles = c.particles;
       r->pruned = (c.stop == 1);
@@ -272,7 +343,7 @@ int or_sums(const or_params* p, const double* points, int64_t n_points, double t
     double* row = sums + i * nb * 3;
     for (int64_t q = 0; q < n_trees; ++q) {
       tree_ctx c = {p, &nz, seed, i, j0 + q, 0, 0, 0, 0};
-      double C = particle(&c, points + i * p->dim, t, 1u);
+      double C = root_factor(p, &nz, t) * particle(&c, points + i * p->dim, t, 1u);
       s.trees++;
       s.particles += c.particles;
       s.leaves += c.leaves;

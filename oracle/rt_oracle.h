@@ -31,6 +31,17 @@ typedef struct {
   double  init_scale;
   int32_t K;            /* orders 0..K kept */
   int32_t precision;    /* ignored by the oracle (FP64 throughout) */
+  /* --- NEXT rows f2/f3 --------------------------------- */
+  int32_t strategy;     /* 0: exponential clock with the potential -λu (default);
+                           1: Strategy A with the shift u = v e^{λt};
+                           2: Strategy B, Bernoulli leaves + uniform split times
+                               */
+  double  q;            /* Strategy B: P(ξ = 0) = probability a particle is a leaf */
+  int32_t coef_kind[9]; /* per power k: 0 b_k constant; 1 b_k e^{-x_a²/s²}/(t + t0)
+                           (Example 5) */
+  int32_t coef_axis;    /* a */
+  double  coef_scale;   /* s > 0 */
+  double  coef_t0;      /* t0 > 0 */
 } or_params;
 
 typedef struct {
@@ -40,8 +51,10 @@ typedef struct {
   int32_t  support[9];     /* k values, ascending */
   uint64_t thresh[9];      /* integer thresholds T_k (last = 2^32) */
   double   p_hat[9];       /* effective probabilities */
-  double   w[9];           /* weights a_k / (λ p̂_k) */
+  double   w[9];           /* weights a_k / (λ p̂_k); Strategy B: a_k / ((1 - q̂) p̂_k) */
   int32_t  beta;           /* bits per child digit in labels */
+  uint64_t tq;             /* Strategy B: leaf iff 32-bit draw < tq (q̂ = tq / 2^32) */
+  double   q_hat;          /* Strategy B: effective leaf probability */
 } or_norm;
 
 typedef struct {

@@ -126,3 +126,50 @@ def fd_solve_1d(b, g, t: float, D: float = 1.0, L: float = 12.0, dx: float = 0.0
 def fd_at(b, g, t: float, pts, **kw) -> np.ndarray:
     x, u = fd_solve_1d(b, g, t, **kw)
     return np.interp(np.asarray(pts, dtype=np.float64), x, u)
+
+
+def fd_solve_1d_xt(fxt, g, t: float, D: float = 1.0, L: float = 12.0, dx: float = 0.02,
+                   dt: float = 2e-3) -> tuple[np.ndarray, np.ndarray]:
+    """As fd_solve_1d for a reaction f(u, x, t) depending on space and time
+    (variable coefficients): Strang splitting, the reaction
+    half-steps integrated by RK4 in time at fixed x, CN diffusion."""
+    x = np.arange(-L, L + 0.5 * dx, dx)
+    n = x.size
+    u = g(x).astype(np.float64)
+    nsteps = int(round(t / dt))
+    dt = t / nsteps
+    r = D * dt / dx ** 2
+    m = n - 2
+    ab = np.zeros((3, m))
+    ab[0, 1:] = -0.5 * r
+    ab[1, :] = 1.0 + r
+    ab[2, :-1] = -0.5 * r
+
+    def react(v, t0, h):
+        sub = 4
+        hh = h / sub
+        tt = t0
+        for _ in range(sub):
+            k1 = fxt(v, x, tt)
+            k2 = fxt(v + 0.5 * hh * k1, x, tt + 0.5 * hh)
+            k3 = fxt(v + 0.5 * hh * k2, x, tt + 0.5 * hh)
+            k4 = fxt(v + hh * k3, x, tt + hh)
+            v = v + hh / 6.0 * (k1 + 2 * k2 + 2 * k3 + k4)
+            tt += hh
+        return v
+
+    for s in range(nsteps):
+        t0 = s * dt
+        u = react(u, t0, 0.5 * dt)
+        ul, ur = u[0], u[-1]
+        rhs = u[1:-1] + 0.5 * r * (u[:-2] - 2 * u[1:-1] + u[2:])
+        rhs[0] += 0.5 * r * ul
+        rhs[-1] += 0.5 * r * ur
+        inner = solve_banded((1, 1), ab, rhs)
+        u = np.concatenate([[ul], inner, [ur]])
+        u = react(u, t0 + 0.5 * dt, 0.5 * dt)
+    return x, u
+
+
+def catalan(n: int) -> int:
+    return math.comb(2 * n, n) // (n + 1)

@@ -72,12 +72,24 @@ def plane_nodes(dim: int, planes: List[dict], max_points: int) -> np.ndarray:
     return np.array(out, dtype=np.float64).reshape(-1, dim)
 
 
+STRAT_POTENTIAL, STRAT_A_SHIFT, STRAT_B = 0, 1, 2
+COEF_CONST, COEF_GAUSS_RATIONAL = 0, 1
+
+
 def _eq(dim, b, g_kind, g_amp, g_scale, K, D=1.0, lam=0.0,
-        offspring=OFFSPRING_ABS, precision=PREC_FP64) -> dict:
+        offspring=OFFSPRING_ABS, precision=PREC_FP64, strategy=STRAT_POTENTIAL, q=0.5,
+        coef_kind=None, coef_axis=0, coef_scale=1.0, coef_t0=0.1) -> dict:
+    """Equation parameters (the fields of rt_eq_params / or_params).
+
+    strategy: 0 exponential clock with potential -λu; 1 Strategy A with the
+    shift u = v e^{λt}; 2 Strategy B (q = P(leaf)).  coef_kind[k] = 1 makes the
+    coefficient of u^k variable: b_k exp(-x_a²/s²)/(t + t0) (Example 5)."""
     bb = list(b) + [0.0] * (9 - len(b))
+    ck = list(coef_kind) + [0] * (9 - len(coef_kind)) if coef_kind else [0] * 9
     return dict(dim=dim, D=D, degree=len(b) - 1, b=bb, lam=lam,
                 offspring=offspring, init_kind=g_kind, init_amp=g_amp,
-                init_scale=g_scale, K=K, precision=precision)
+                init_scale=g_scale, K=K, precision=precision, strategy=strategy, q=q,
+                coef_kind=ck, coef_axis=coef_axis, coef_scale=coef_scale, coef_t0=coef_t0)
 
 
 # BASELINE.json "configs" (SURVEY.md §8(d) table).  b = (b_0, b_1, ...) with
