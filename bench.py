@@ -48,11 +48,15 @@ LD = dict(log=30, exp=18, sqrt=8, div=8, tanh=37, sincospi=25, cospi=16, u2d=1)
 
 def algo_fp64_per_unit(eq: dict) -> dict:
     d = eq["dim"]
+    strat = eq.get("strategy", 0)
     unif = LD["u2d"] + 1                                   # (double)m * 2^-53
     pair_both = 2 * unif + LD["log"] + 1 + LD["sqrt"] + 1 + LD["sincospi"] + 2
     pair_cos = 2 * unif + LD["log"] + 1 + LD["sqrt"] + 1 + LD["cospi"] + 1
-    per_particle = (unif + LD["log"] + 1        # S = -log(U) * (1/λ)
-                    + 1                          # S > τ
+    if strat == 2:                                         # Strategy B: ξ integer test,
+        clock = unif + 3                                   # h = τS, τ_c = τ(1 - S)
+    else:
+        clock = unif + LD["log"] + 1 + 1                   # S = -log(U)/λ, S > τ
+    per_particle = (clock
                     + LD["sqrt"] + 1             # σ sqrt(h)
                     + d)                         # y_k + (σ√h) ξ_k
     per_particle += {1: pair_cos, 2: pair_both, 3: pair_both + pair_cos}[d]
@@ -61,9 +65,17 @@ def algo_fp64_per_unit(eq: dict) -> dict:
          W.G_TANH_STEP: LD["div"] + LD["tanh"] + 1 + 2,
          W.G_GAUSS: r2 + LD["div"] + LD["exp"] + 1,
          W.G_LORENTZ: r2 + LD["div"] + 1 + LD["div"]}[eq["init_kind"]]
-    return dict(particle=per_particle, leaf=g + 1,   # Π *= g
-                split=2,                             # Π *= w_k, τ − S
-                tree=3)                              # C², ΣC, ΣC²
+    split = 2                                            # Π *= w_k, τ_c
+    if strat == 1:
+        split += LD["exp"] + 2                           # e^{(k-1)λτ_c}
+    if strat == 2:
+        split += 1                                       # η(τ) = τ
+    if any(eq.get("coef_kind", [0] * 9)):
+        split += LD["exp"] + LD["div"] + 4               # e^{-y²/s²}/(τ_c + t0)
+    return dict(particle=per_particle,
+                leaf=g + 1 + (1 if strat == 2 else 0),   # Π *= g (/ q)
+                split=split,
+                tree=3 + (1 if strat == 1 else 0))       # C², ΣC, ΣC² (× e^{λt})
 
 
 def algo_fp64_ops(eq: dict, stats: dict) -> float:

@@ -64,6 +64,22 @@ typedef enum {
   RT_G_LORENTZ = 3     /* g = amp / (1 + |x|^2 / scale^2)           */
 } rt_init;
 
+/* How a tree samples the Duhamel form of the PDE:
+ *  RT_STRATEGY_POTENTIAL: f = −λu + Σ a_k u^k, exponential clock of rate λ,
+ *    weights a_k/(λ p_k) (the hot path's default);
+ *  RT_STRATEGY_A_SHIFT:   Strategy A with u = v e^{λt}:
+ *    weights b_k e^{(k−1)λτ_c}/(λ p_k) at a split whose children have
+ *    horizon τ_c, e^{λt} per tree;
+ *  RT_STRATEGY_B:         Strategy B: a particle is a leaf
+ *    with probability q (weight g/q), else splits after the uniform fraction S
+ *    of its horizon τ with weight τ b_k/((1−q) p_k), children horizon τ(1−S). */
+typedef enum { RT_STRATEGY_POTENTIAL = 0, RT_STRATEGY_A_SHIFT = 1, RT_STRATEGY_B = 2 } rt_strategy;
+
+/* Coefficient of u^k: constant b_k, or b_k e^{−x_a²/s²}/(t + t0) evaluated at
+ * the split position and the children's time argument τ_c (Example 5,
+ * PAPER.md:1084-1088).  Not allowed on k = 1 with RT_STRATEGY_POTENTIAL. */
+typedef enum { RT_COEF_CONST = 0, RT_COEF_GAUSS_RATIONAL = 1 } rt_coef;
+
 typedef enum {
   RT_PREC_FP64 = 0,       /* everything FP64                                     */
   RT_PREC_FP32_POS = 1    /* FP32 positions, increments and g; FP64 clock, weights,
@@ -83,6 +99,13 @@ typedef struct {
   int32_t K;            /* orders 0..K are kept; trees with Ne > K are pruned.     */
                         /* 0 <= K <= 30 and 1 + K*β <= 56 (β = child-digit bits)   */
   int32_t precision;    /* rt_precision                                            */
+  /* --- NEXT rows f2 / f3; zero-initialised = the default path --- */
+  int32_t strategy;     /* rt_strategy                                             */
+  double  q;            /* RT_STRATEGY_B: P(leaf) = P(ξ = 0), 0 < q < 1             */
+  int32_t coef_kind[9]; /* per power k: rt_coef (variable c_k(x,t))  */
+  int32_t coef_axis;    /* a: the coordinate of the variable factor                */
+  double  coef_scale;   /* s > 0                                                   */
+  double  coef_t0;      /* t0 > 0                                                  */
 } rt_eq_params;
 
 typedef struct {
@@ -120,7 +143,10 @@ typedef struct rt_handle rt_handle;
  * RT_E_ARG on: null pointers, dim ∉ {1,2,3}, D <= 0 or non-finite, degree ∉
  * [0,8], non-finite b/λ/amp/scale, scale <= 0, K ∉ [0,30], label width
  * 1 + K*β > 56, a support category of zero integer width, an unknown enum,
- * an unknown precision.  An empty support (purely linear f) is legal. */
+ * an unknown precision, RT_STRATEGY_B with q ∉ (0,1) (or a zero-width integer
+ * threshold), a variable coefficient with s <= 0, t0 <= 0, an axis outside
+ * [0, dim), or on k = 1 under RT_STRATEGY_POTENTIAL, RT_PREC_FP32_POS with a
+ * strategy other than RT_STRATEGY_POTENTIAL.  An empty support (purely linear f) is legal. */
 rt_status rt_create(const rt_eq_params* params, rt_handle** out);
 
 /* Free the handle and its device scratch.  NULL is a no-op. */

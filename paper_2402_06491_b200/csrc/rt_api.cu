@@ -74,6 +74,8 @@ struct Norm {
   uint64_t thresh[9];
   double w[9];
   int beta;
+  uint32_t tq;     // Strategy B: leaf iff the 32-bit draw < tq (q̂ = tq / 2^32)
+  double q_hat;
 };
 
 struct rt_handle {
@@ -98,15 +100,18 @@ struct rt_handle {
 // (R2, R9).  λ default: −b_1 if b_1 < 0 else 1 (R3).
 static rt_status normalize(const rt_eq_params& p, Norm& o) {
   std::memset(&o, 0, sizeof(o));
+  const bool pot = p.strategy == RT_STRATEGY_POTENTIAL;
   double lam = p.lambda;
-  if (!(lam > 0.0)) lam = (p.b[1] < 0.0) ? -p.b[1] : 1.0;
+  // potential form: λ = −b_1 if b_1 < 0 else 1 (R3); the shift
+  // u = v e^{t} of Strategy A uses rate 1 unless overridden
+  if (!(lam > 0.0)) lam = (pot && p.b[1] < 0.0) ? -p.b[1] : 1.0;
   o.lambda = lam;
   o.inv_lambda = 1.0 / lam;
   o.sigma = std::sqrt(2.0 * p.D);
   int kmax = 0, ns = 0;
   for (int k = 0; k <= 8; ++k) {
     double a = (k <= p.degree) ? p.b[k] : 0.0;
-    if (k == 1) a += lam;
+    if (k == 1 && pot) a += lam;      // only the potential form moves −λu out of f
     o.a[k] = a;
     if (a != 0.0) {
       o.support[ns++] = k;
@@ -117,6 +122,13 @@ static rt_status normalize(const rt_eq_params& p, Norm& o) {
   int beta = 1;
   while ((1 << beta) < kmax) ++beta;
   o.beta = beta;
+  if (p.strategy == RT_STRATEGY_B) {
+    const double tq = std::nearbyint(p.q * 4294967296.0);
+    if (!(tq >= 1.0 && tq < 4294967296.0))
+      return fail(RT_E_ARG, "Strategy B needs 0 < q < 1 with a nonzero 32-bit threshold");
+    o.tq = static_cast<uint32_t>(tq);
+    o.q_hat = tq / 4294967296.0;
+  }
   if (ns == 0) return RT_OK;
   double prob[9];
   if (p.offspring == RT_OFFSPRING_UNIFORM) {
@@ -137,7 +149,9 @@ static rt_status normalize(const rt_eq_params& p, Norm& o) {
       return fail(RT_E_ARG, "offspring k=%d has zero integer probability width", o.support[s]);
     o.thresh[s] = T;
     const double phat = static_cast<double>(T - prev) / 4294967296.0;
-    o.w[s] = o.a[o.support[s]] / (lam * phat);
+    // c'_α = c_α/p_α; Strategy B: c̃ = c/(1 − q)
+    o.w[s] = o.a[o.support[s]] /
+             ((p.strategy == RT_STRATEGY_B ? (1.0 - o.q_hat) : lam) * phat);
     prev = T;
   }
   return RT_OK;
@@ -164,6 +178,23 @@ extern "C" rt_status rt_create(const rt_eq_params* params, rt_handle** out) {
   if (p.K < 0 || p.K > 30) return fail(RT_E_ARG, "K must be in [0, 30] (got %d)", p.K);
   if (p.precision != RT_PREC_FP64 && p.precision != RT_PREC_FP32_POS)
     return fail(RT_E_ARG, "unknown precision %d", p.precision);
+  if (p.strategy < RT_STRATEGY_POTENTIAL || p.strategy > RT_STRATEGY_B)
+    return fail(RT_E_ARG, "unknown strategy %d", p.strategy);
+  if (p.precision == RT_PREC_FP32_POS && p.strategy != RT_STRATEGY_POTENTIAL)
+    return fail(RT_E_ARG, "the FP32-position variant exists for RT_STRATEGY_POTENTIAL only");
+  bool any_var = false;
+  for (int k = 0; k <= 8; ++k) {
+    if (p.coef_kind[k] != RT_COEF_CONST && p.coef_kind[k] != RT_COEF_GAUSS_RATIONAL)
+      return fail(RT_E_ARG, "unknown coef_kind[%d] = %d", k, p.coef_kind[k]);
+    any_var = any_var || p.coef_kind[k] == RT_COEF_GAUSS_RATIONAL;
+  }
+  if (any_var) {
+    if (p.strategy == RT_STRATEGY_POTENTIAL && p.coef_kind[1] != RT_COEF_CONST)
+      return fail(RT_E_ARG, "a variable coefficient on k = 1 needs a strategy without the potential");
+    if (!(p.coef_scale > 0.0) || !is_fin(p.coef_scale) || !(p.coef_t0 > 0.0) ||
+        !is_fin(p.coef_t0) || p.coef_axis < 0 || p.coef_axis >= p.dim)
+      return fail(RT_E_ARG, "variable coefficient needs scale > 0, t0 > 0, 0 <= axis < dim");
+  }
   Norm nz;
   rt_status s = normalize(p, nz);
   if (s != RT_OK) return s;
@@ -216,25 +247,29 @@ extern "C" rt_status rt_set_pool(rt_handle* h, int32_t pool_entries) {
 // tree-walk launch (rows a3–a7)
 using KernelFn = void (*)(WalkParams);
 
-template <int DIM, int GK, bool REC, bool F32>
+template <int DIM, int GK, bool REC, bool F32, bool SB>
 static KernelFn pick_kernel() {
-  return rtk::tree_walk_kernel<DIM, GK, REC, F32>;
+  return rtk::tree_walk_kernel<DIM, GK, REC, F32, SB>;
 }
 
 // The kernel for (dim, g, rec) and the production (rec = false) kernel whose
 // occupancy fixes the launch geometry for both.
-static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, KernelFn* prod, int* smem,
-                           int* pool_cap) {
+static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, bool sb, KernelFn* prod,
+                           int* smem, int* pool_cap) {
 #define RT_K(D, G)                                                              \
   if (dim == D && gk == G) {                                                    \
     *smem = rtk::smem_bytes<D>();                                               \
     *pool_cap = rtk::PoolCap<D>::v;                                             \
-    if (f32) {                                                                  \
-      *prod = pick_kernel<D, G, false, true>();                                 \
-      return rec ? pick_kernel<D, G, true, true>() : *prod;                     \
+    if (sb) {                                                                   \
+      *prod = pick_kernel<D, G, false, false, true>();                          \
+      return rec ? pick_kernel<D, G, true, false, true>() : *prod;              \
     }                                                                           \
-    *prod = pick_kernel<D, G, false, false>();                                  \
-    return rec ? pick_kernel<D, G, true, false>() : *prod;                      \
+    if (f32) {                                                                  \
+      *prod = pick_kernel<D, G, false, true, false>();                          \
+      return rec ? pick_kernel<D, G, true, true, false>() : *prod;              \
+    }                                                                           \
+    *prod = pick_kernel<D, G, false, false, false>();                           \
+    return rec ? pick_kernel<D, G, true, false, false>() : *prod;               \
   }
   RT_K(1, 0) RT_K(1, 1) RT_K(1, 2) RT_K(1, 3)
   RT_K(2, 0) RT_K(2, 1) RT_K(2, 2) RT_K(2, 3)
@@ -368,7 +403,7 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   int smem = 0, pool_cap = 0;
   KernelFn prod = nullptr;
   KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, p.precision == RT_PREC_FP32_POS,
-                           &prod, &smem, &pool_cap);
+                           p.strategy == RT_STRATEGY_B, &prod, &smem, &pool_cap);
   if (!fn) return fail(RT_E_ARG, "no kernel for dim=%d init_kind=%d", p.dim, p.init_kind);
   if (smem > 48 * 1024) {
     RT_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -405,6 +440,18 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
     P.kval[q] = nz.support[q];
   }
   P.n_support = nz.n_support;
+  // f2/f3 weight factors
+  P.var_s = 0u;
+  for (int q = 0; q < nz.n_support; ++q)
+    if (p.coef_kind[nz.support[q]] == RT_COEF_GAUSS_RATIONAL) P.var_s |= 1u << q;
+  P.wmode = (P.var_s != 0u ? 1 : 0) | (p.strategy == RT_STRATEGY_A_SHIFT ? 2 : 0);
+  P.lam = nz.lambda;
+  P.root = p.strategy == RT_STRATEGY_A_SHIFT ? std::exp(nz.lambda * t) : 1.0;   // u = v e^{λt}
+  P.coef_axis = p.coef_axis;
+  P.coef_inv_s2 = 1.0 / (p.coef_scale * p.coef_scale);
+  P.coef_t0 = p.coef_t0;
+  P.tq = nz.tq;
+  P.inv_q = p.strategy == RT_STRATEGY_B ? 1.0 / nz.q_hat : 1.0;
   P.beta = nz.beta;
   P.K = p.K;
   P.nb = nb;

@@ -84,6 +84,16 @@ struct WalkParams {
   int64_t n_rec;
   unsigned long long* stats;   // trees, pruned, particles, leaves, splits
   unsigned int* task_ctr;      // dynamic task counter (zeroed before the launch)
+  // NEXT rows f2/f3: split-weight factors beyond the constant
+  // w_k — bit0 variable coefficients, bit1 Strategy A's e^{(k-1)λτ_c} (0 on
+  // the default path: one warp-uniform test per iteration)
+  int32_t wmode;
+  uint32_t var_s;              // bit s: support entry s has a variable coefficient
+  double lam, root;            // λ; per-tree root factor (e^{λt} with the shift, else 1)
+  int32_t coef_axis;
+  double coef_inv_s2, coef_t0;
+  uint32_t tq;                 // Strategy B: leaf iff block-0 word 3 < tq
+  double inv_q;                // Strategy B: 1/q̂
   unsigned long long* wtime;   // debug (RT_WARP_TIMES): [warps][4] start, end, smid, iterations; or null
 };
 
@@ -153,7 +163,10 @@ __host__ __device__ constexpr int smem_bytes() {
 // configs[4]): the clock S, the leaf test, horizons, weights, the tree
 // product and all sums stay FP64 (tree structure identical to the FP64
 // path); positions, the Brownian increment and g are single precision.
-template <int DIM, int GK, bool REC, bool F32>
+// SB = Strategy B: a particle is a leaf with probability
+// q (ξ = 0, weight g/q), else it splits after the uniform fraction S of its
+// horizon with weight τ c_k/((1-q) p_k) and its children inherit τ(1-S).
+template <int DIM, int GK, bool REC, bool F32, bool SB>
 __global__ void __launch_bounds__(kThreads, MinCtas<DIM, REC>::v)
 tree_walk_kernel(const __grid_constant__ WalkParams P) {
   using PT = typename std::conditional<F32, float, double>::type;   // position type
@@ -247,7 +260,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     tj = j;
 #pragma unroll
     for (int k = 0; k < DIM; ++k) y[k] = static_cast<PT>(ws->iss_y[k]);
-    tau = P.t; label = 1; Pi = 1.0; ne = 0; top = -1;
+    tau = P.t; label = 1; Pi = P.root; ne = 0; top = -1;
     if constexpr (REC) { leaves = 0; parts = 0; }
     active = true;
   };
@@ -350,12 +363,21 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const uint32_t c3 = static_cast<uint32_t>(label >> 32);
     const uint4 r0 = philox4x32_10(tj, ti, c2, c3, P.rk);
     const uint4 r1 = philox4x32_10(tj, ti, c2, c3 | (1u << 24), P.rk);
-    // exponential clock S ~ λ e^{-λS}
-    const double S = -log_tab(unif53(r0.x, r0.y), ltab) * P.inv_lambda;
-    const bool leaf = S > tau;                  // 1{S > t}
-    const double h2d = (leaf ? tau : S) * P.two_d;   // variance 2D·h of the increment
-    // Box–Muller with the lifetime folded into the radius (R8):
-    // y ← y + σ sqrt(h) · sqrt(-2 log v1) · (cos, sin)(2π v2), in place
+    bool leaf;
+    double tc, h2d;                             // children's horizon, 2D·lifetime
+    if constexpr (SB) {
+      // ξ = 0 (leaf) iff block-0 word 3 < tq; S ~ U(0,1) the split fraction
+      leaf = r0.w < P.tq;
+      const double Sf = unif53(r0.x, r0.y);
+      h2d = (leaf ? tau : tau * Sf) * P.two_d;
+      tc = tau * (1.0 - Sf);
+    } else {
+      // exponential clock S ~ λ e^{-λS}
+      const double S = -log_tab(unif53(r0.x, r0.y), ltab) * P.inv_lambda;
+      leaf = S > tau;                           // 1{S > t}
+      h2d = (leaf ? tau : S) * P.two_d;         // variance 2D·h of the increment
+      tc = tau - S;
+    }
     if constexpr (F32) {
       // the same draws and formula in single precision, on the MUFU
       // approximations (lg2, sin/cos at |x| <= π, rsqrt seeds: ~2^-21)
@@ -402,10 +424,18 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       // d = 3 from the same two blocks (R8): radii uniforms from
       // block-1 (w1:w0), (w3:w2); angles from 32-bit uniforms — block-0 w3 and
       // the word of the 12 low bits the 53-bit uniforms leave unused
-      const double v1 = unif53(r1.x, r1.y), v2 = unif32(r0.w);
+      const double v1 = unif53(r1.x, r1.y);
       const double v3 = unif53(r1.z, r1.w);
-      const uint32_t w4 = ((r0.x & 0xFFFu) << 20) | ((r1.x & 0xFFFu) << 8) | ((r1.z & 0xFFFu) >> 4);
-      const double v4 = unif32(w4);
+      double v2, v4;
+      if constexpr (SB) {                        // block-0 word 3 is ξ: angles from block 2
+        const uint4 r2 = philox4x32_10(tj, ti, c2, c3 | (2u << 24), P.rk);
+        v2 = unif32(r2.x);
+        v4 = unif32(r2.y);
+      } else {
+        const uint32_t w4 = ((r0.x & 0xFFFu) << 20) | ((r1.x & 0xFFFu) << 8) | ((r1.z & 0xFFFu) >> 4);
+        v2 = unif32(r0.w);
+        v4 = unif32(w4);
+      }
       const double rad = sqrt_nr(-2.0 * log_tab(v1, ltab) * h2d);
       double sn, cs;
       sincospi2(2.0 * v2, sn, cs);
@@ -426,7 +456,22 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     if constexpr (F32) gv = static_cast<double>(g_eval_f<DIM, GK>(y, P));
     else gv = g_eval<DIM, GK>(y, P);
     const int k = ktab[s];
-    const double wk = wtab[s];
+    double wk = wtab[s];
+    if constexpr (SB) wk *= tau;                // η(τ) = τ
+    if (P.wmode != 0) {                         // warp-uniform: f2/f3 weight factors
+      double f = 1.0;
+      if ((P.var_s >> s) & 1u) {                // c_k(y, τ_c) = b_k e^{-y_a²/s²}/(τ_c + t0)
+        double ya = static_cast<double>(y[0]);   // (no dynamic register indexing)
+        if constexpr (DIM >= 2) if (P.coef_axis == 1) ya = static_cast<double>(y[1]);
+        if constexpr (DIM >= 3) if (P.coef_axis == 2) ya = static_cast<double>(y[2]);
+        f = exp_neg(-(ya * ya) * P.coef_inv_s2) * rcp_nr(tc + P.coef_t0);
+      }
+      if (P.wmode & 2) {                        // e^{(k-1)λτ_c}
+        const double a = static_cast<double>(k - 1) * P.lam * tc;
+        f *= a >= 0.0 ? rcp_nr(exp_neg(-a)) : exp_neg(a);
+      }
+      wk *= f;
+    }
 
     // ---------------- tree logic: predicated straight-line code ---------------
     const bool split = active && !leaf;
@@ -435,7 +480,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const bool kill = split && !pruned && P.n_support == 0;   // purely linear f
     const bool branch = split && !pruned && !kill;
     // g at a leaf; h^(α) = c'_α at a split; 0 if killed
-    const double fac = leaf ? gv : (kill ? 0.0 : wk);
+    const double fac = leaf ? (SB ? gv * P.inv_q : gv) : (kill ? 0.0 : wk);
     if (active) Pi *= fac;
     c_part += active ? 1u : 0u;
     c_leaf += (active && leaf) ? 1u : 0u;
@@ -447,9 +492,9 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const bool pop = (active && leaf) || (branch && k == 0);
     const bool has = pop && top >= 0;            // resume the top group's next child
     const bool done = pruned || kill || (pop && top < 0);
-    // child 0 continues from the split point y with horizon τ − S (popping
+    // child 0 continues from the split point y with horizon τ_c (popping
     // lanes overwrite y, τ, label below; finished lanes are re-initialised)
-    tau -= S;
+    tau = tc;
     const uint64_t base = label << P.beta;
     const uint64_t push_pk = (base | 1ull) | (static_cast<uint64_t>(k - 1) << 56);
     label = base;

@@ -37,7 +37,9 @@ class EqParams(C.Structure):
     _fields_ = [("dim", C.c_int32), ("D", C.c_double), ("degree", C.c_int32),
                 ("b", C.c_double * 9), ("lam", C.c_double), ("offspring", C.c_int32),
                 ("init_kind", C.c_int32), ("init_amp", C.c_double), ("init_scale", C.c_double),
-                ("K", C.c_int32), ("precision", C.c_int32)]
+                ("K", C.c_int32), ("precision", C.c_int32),
+                ("strategy", C.c_int32), ("q", C.c_double), ("coef_kind", C.c_int32 * 9),
+                ("coef_axis", C.c_int32), ("coef_scale", C.c_double), ("coef_t0", C.c_double)]
 
 
 class Stats(C.Structure):
@@ -134,6 +136,14 @@ def eq_params(eq: dict) -> EqParams:
     p.init_kind = eq["init_kind"]; p.init_amp = eq["init_amp"]
     p.init_scale = eq.get("init_scale", 1.0); p.K = eq["K"]
     p.precision = eq.get("precision", PREC_FP64)
+    p.strategy = eq.get("strategy", 0)
+    p.q = eq.get("q", 0.5)
+    ck = eq.get("coef_kind", [0] * 9)
+    for k in range(9):
+        p.coef_kind[k] = ck[k]
+    p.coef_axis = eq.get("coef_axis", 0)
+    p.coef_scale = eq.get("coef_scale", 1.0)
+    p.coef_t0 = eq.get("coef_t0", 0.1)
     return p
 
 

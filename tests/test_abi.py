@@ -58,6 +58,11 @@ def _create(rtmod, **kw):
     (dict(precision=2), "precision"), (dict(init_amp=float("inf")), "init_amp"),
     (dict(K=28), "label width"),                       # β = 2 for k_max = 4: 1 + 28*2 > 56
     (dict(b=[0, -1, 1e-12, 1.0] + [0] * 5, degree=3), "zero integer"),
+    (dict(strategy=3), "strategy"), (dict(strategy=2, q=0.0), "q < 1"),
+    (dict(strategy=2, q=1.0), "q < 1"), (dict(strategy=1, precision=1), "FP32"),
+    (dict(coef_kind=[0, 1] + [0] * 7), "k = 1"), (dict(coef_kind=[0, 0, 2] + [0] * 6), "coef_kind"),
+    (dict(coef_kind=[0, 0, 1] + [0] * 6, coef_t0=0.0), "t0 > 0"),
+    (dict(coef_kind=[0, 0, 1] + [0] * 6, coef_axis=1), "axis"),
 ])
 def test_create_rejects(rtmod, kw, frag):
     st, msg = _create(rtmod, **kw)

@@ -92,6 +92,9 @@ def test_philox_vs_curand_and_oracle(P, orc):
 
 # ----------------------------------------------------------------------------
 # per-tree parity (structure bit-exact, C to 1e-12) and per-node parity
+GN = 1.0 / (4.0 * np.pi) ** 0.5          # Examples 1, 5: e^{-x^2/4}/sqrt(4 pi)
+
+
 def _eq_variants():
     base2 = W.get("cfg2")["eq"]
     lin = dict(base2, degree=1, b=[0.0, -1.0] + [0.0] * 7)
@@ -111,6 +114,25 @@ def _eq_variants():
         "d3_gauss": (dict(W.get("cfg4")["eq"], init_kind=W.G_GAUSS, init_scale=1.5, D=0.7), W.random_nodes(12, 3, 4), 0.8, 1_000),
         "d2_lorentz": (dict(W.get("cfg3")["eq"], init_kind=W.G_LORENTZ, init_scale=0.8), W.random_nodes(12, 2, 5), 0.6, 1_000),
         "d1_const_lam": (dict(base2, init_kind=W.G_CONST, init_amp=0.4, lam=1.7), W.random_nodes(6, 1, 6), 1.0, 2_000),
+        # NEXT rows f2 / f3
+        "shift_ex1": (W._eq(1, (0.0, 0.0, -1.0), W.G_GAUSS, GN, 2.0, K=12, strategy=W.STRAT_A_SHIFT),
+                      W.random_nodes(8, 1, 7), 0.5, 3_000),
+        "shift_ex5_d2": (W._eq(2, (0.0, 0.0, -1.0), W.G_GAUSS, GN, 2.0, K=12, strategy=W.STRAT_A_SHIFT,
+                               coef_kind=[0, 0, 1], coef_axis=0, coef_scale=1.0, coef_t0=0.1),
+                         W.random_nodes(8, 2, 8), 0.5, 2_000),
+        "shift_k01_d3": (W._eq(3, (0.1, -0.5, -1.0, 0.3), W.G_LORENTZ, 0.5, 1.0, K=10,
+                               strategy=W.STRAT_A_SHIFT, lam=1.3), W.random_nodes(6, 3, 9), 0.8, 800),
+        "B_ex3": (W._eq(1, (0.0, 0.0, -1.25, -1.0), W.G_TANH_STEP, 1.0, 2.0 * 2 ** 0.5, K=14,
+                        strategy=W.STRAT_B, q=0.6), W.random_nodes(8, 1, 10), 0.3, 3_000),
+        "B_cfg2_k1": (dict(W._eq(1, W.B_CFG2, W.G_GAUSS, 0.4, 1.0, K=12, strategy=W.STRAT_B, q=0.7)),
+                      W.random_nodes(8, 1, 11), 1.0, 2_000),
+        "B_d3_var": (W._eq(3, (0.0, 0.0, -1.0, 0.5), W.G_GAUSS, 0.5, 1.2, K=12, strategy=W.STRAT_B, q=0.65,
+                           coef_kind=[0, 0, 1, 1], coef_axis=2, coef_scale=1.5, coef_t0=0.2),
+                     W.random_nodes(6, 3, 12), 0.7, 1_000),
+        "B_d2_uniform": (W._eq(2, (0.0, 0.0, 0.6, 0.4), W.G_LORENTZ, 0.6, 1.0, K=12, strategy=W.STRAT_B,
+                               q=0.7, offspring=W.OFFSPRING_UNIFORM), W.random_nodes(6, 2, 13), 0.5, 1_500),
+        "pot_var": (dict(base2, coef_kind=[0, 0, 1, 0, 1, 0, 0, 0, 0], coef_axis=0, coef_scale=2.0, coef_t0=0.3),
+                    W.random_nodes(6, 1, 14), 1.0, 2_000),
     }
 
 
@@ -137,7 +159,8 @@ def test_tree_parity(P, orc, name):
         assert st["particles"] == st_ref["particles"] and st["leaves"] == st_ref["leaves"]
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg2_uniform", "poisson_k1"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg2_uniform", "poisson_k1",
+                                  "shift_ex5_d2", "B_ex3", "B_d3_var"])
 def test_estimate_parity(P, orc, name):
     eq, pts, t, N = CASES[name]
     N = max(N, 2)
@@ -192,7 +215,8 @@ def test_geometry_and_determinism(P):
     assert_nodes_close(d[:, :, 0], a[:, :, 0], rtol=1e-12, what="one CTA")
 
 
-@pytest.mark.parametrize("name,pool", [("cfg4", 1), ("cfg4", 9), ("cfg2_t2", 3), ("d3_gauss", 40)])
+@pytest.mark.parametrize("name,pool", [("cfg4", 1), ("cfg4", 9), ("cfg2_t2", 3), ("d3_gauss", 40),
+                                       ("B_d3_var", 2)])
 def test_stack_pool_overflow(P, orc, name, pool):
     """A small shared-memory stack pool pushes pending sibling groups to the
     global overflow area; trees must still equal the oracle's, and the sums
@@ -427,3 +451,42 @@ def test_full_cfg2_closed_form_and_fd(P):
     ref = cf.fd_at(eq["b"][:5], lambda x: 0.4 * np.exp(-x * x), t, xs)
     for q, i in enumerate([0, 21, 32, 42]):
         assert abs(u[i] - ref[q]) < 4.0 * ses[i] + 2e-6, (xs[q], u[i], ref[q], ses[i])
+
+
+@pytest.mark.parametrize("name", ["ex1A", "ex1B", "ex3A", "ex3B"])
+def test_examples_gpu_vs_fd(P, name):
+    """NEXT rows f2/f3 at scale: the paper's Examples 1 and 3
+    on 16 nodes x 2e5 trees through the CUDA path, partial sums Σ c_n against
+    Crank-Nicolson finite differences within 4 standard errors (R22)."""
+    import closed_forms as cf
+    cfg = W.get(name)
+    eq, t = cfg["eq"], cfg["t"]
+    xs = W.linspace(-3.0, 3.0, 16)
+    est = P.Estimator(eq)
+    s = est.sums(dev(xs[:, None]), t, 200_000, seed=2024)
+    c, se, us, ses = P.finalize(s, eq["K"], 200_000)
+    if eq["init_kind"] == W.G_GAUSS:
+        g = lambda x: eq["init_amp"] * np.exp(-x * x / eq["init_scale"] ** 2)   # noqa: E731
+    else:
+        g = lambda x: eq["init_amp"] * 0.5 * (1.0 + np.tanh(x / eq["init_scale"]))   # noqa: E731
+    ref = cf.fd_at(eq["b"][: eq["degree"] + 1], g, t, xs, dx=0.02, dt=1e-3)
+    z = (us.cpu().numpy() - ref) / ses.cpu().numpy()
+    assert np.all(np.abs(z) < 4.0), z
+
+
+def test_example5_gpu_vs_fd_1d_slice(P):
+    """Example 5's variable coefficient e^{-x^2}/(t + 0.1),
+    1-D analogue through the CUDA path (Strategy A shift and B) against FD."""
+    import closed_forms as cf
+    t = 0.5
+    xs = W.linspace(-2.0, 2.0, 9)
+    x, u = cf.fd_solve_1d_xt(lambda v, xx, tt: -np.exp(-xx * xx) / (tt + 0.1) * v * v,
+                             lambda xx: GN * np.exp(-xx * xx / 4.0), t, dx=0.02, dt=1e-3)
+    ref = np.interp(xs, x, u)
+    for strat in (W.STRAT_A_SHIFT, W.STRAT_B):
+        eq = W._eq(1, (0.0, 0.0, -1.0), W.G_GAUSS, GN, 2.0, K=12, strategy=strat, q=2.0 / 3.0,
+                   coef_kind=[0, 0, 1], coef_axis=0, coef_scale=1.0, coef_t0=0.1)
+        s = P.Estimator(eq).sums(dev(xs[:, None]), t, 200_000, seed=77)
+        _, _, us, ses = P.finalize(s, eq["K"], 200_000)
+        z = (us.cpu().numpy() - ref) / ses.cpu().numpy()
+        assert np.all(np.abs(z) < 4.0), (strat, z)

@@ -121,6 +121,26 @@ CONFIGS: Dict[str, dict] = {
                  n_trees=10_000_000, seed=0, L=7, M=7),
 }
 
+# NEXT rows f2 / f3: the paper's Examples
+# on the same node layouts, Strategy A with the
+# e^{λt} shift and Strategy B (q = 2/3, inside the admissible range q >= 1/2
+# of a single quadratic term).  Examples 1-2 data read at t = 0
+# (SURVEY C16): e^{-x^2/4}/sqrt(4 pi) = Gaussian with amp 1/sqrt(4 pi), scale 2.
+_GN = 1.0 / (4.0 * 3.141592653589793) ** 0.5
+_EX1 = dict(b=(0.0, 0.0, -1.0), g=(G_GAUSS, _GN, 2.0))
+_EX3 = dict(b=(0.0, 0.0, -1.25, -1.0), g=(G_TANH_STEP, 1.0, 2.0 * 2.0 ** 0.5))
+_EX5 = dict(coef_kind=[0, 0, 1], coef_axis=0, coef_scale=1.0, coef_t0=0.1)
+for _s, _tag in ((STRAT_A_SHIFT, "A"), (STRAT_B, "B")):
+    CONFIGS[f"ex1{_tag}"] = dict(eq=_eq(1, _EX1["b"], *_EX1["g"], K=12, strategy=_s, q=2.0 / 3.0),
+                                t=0.5, nodes=dict(kind="linspace", lo=-3.0, hi=3.0, n=64),
+                                n_trees=1_000_000, seed=0, L=5, M=5)
+    CONFIGS[f"ex3{_tag}"] = dict(eq=_eq(1, _EX3["b"], *_EX3["g"], K=12, strategy=_s, q=0.75),
+                                t=0.5, nodes=dict(kind="linspace", lo=-3.0, hi=3.0, n=64),
+                                n_trees=1_000_000, seed=0, L=5, M=5)
+    CONFIGS[f"ex5{_tag}"] = dict(eq=_eq(2, _EX1["b"], *_EX1["g"], K=12, strategy=_s, q=2.0 / 3.0, **_EX5),
+                                t=0.5, nodes=dict(kind="planes", planes=_CFG3_PLANES, max_points=256),
+                                n_trees=1_000_000, seed=0, L=5, M=5)
+
 # cfg5: throughput sweep on the cfg2 equation (BASELINE.json configs[4]).
 CFG5_NODES = (64, 1024, 16384)
 CFG5_TREES = (10_000, 1_000_000, 10_000_000)
