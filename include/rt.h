@@ -231,6 +231,49 @@ rt_status rt_set_pool(rt_handle* h, int32_t pool_entries);
 rt_status rt_philox_dev(uint64_t key, const uint32_t* d_ctr, int64_t n, uint32_t* d_out,
                         void* stream);
 
+/* ------------------------------------------------------------------------
+ * NEXT row f1 — probabilistic domain decomposition downstream (PAPER.md:936-950,
+ * 1007-1012), d = 2 with constant coefficients: the square
+ * [lo, hi]² is cut by the artificial interfaces x = mid and y = mid
+ * (mid = (lo+hi)/2) into four subdomains.  Six lines carry nodal points s_j =
+ * lo + j (hi−lo)/(n_s−1) at time levels t_k = k T/(n_t−1): 0 interface x = mid
+ * (points (mid, s_j)), 1 interface y = mid ((s_j, mid)), 2 edge x = lo,
+ * 3 edge x = hi ((lo|hi, s_j)), 4 edge y = lo, 5 edge y = hi ((s_j, lo|hi)).
+ * Their values (t_0: g; t_k > 0: the tree walk + Padé) are interpolated by
+ * not-a-knot tensor splines in (s, t) and used as Dirichlet data of four
+ * decoupled Crank–Nicolson (Peaceman–Rachford ADI, Strang-split RK4 reaction)
+ * solves on the grid x_i = lo + i h, h = (hi−lo)/n_cells.  Fields are
+ * [(n_cells+1)²] row-major in x: F[i (n_cells+1) + j] = u(x_i, y_j, T). */
+typedef struct {
+  double   lo, hi;      /* square domain [lo, hi]²                                 */
+  double   T;           /* final time > 0                                          */
+  int32_t  n_cells;     /* grid cells per side, even, 4 <= n_cells <= 1020          */
+  int32_t  n_steps;     /* time steps, Δt = T / n_steps                            */
+  int32_t  n_s, n_t;    /* nodal points per line / time levels, 4 <= n <= 64        */
+  int32_t  boundary;    /* 0: zero Dirichlet on the outer edges; 1: probabilistic   */
+                        /* values there too                    */
+  int32_t  L, M;        /* Padé order of the nodal values (L + M <= K)             */
+  int64_t  n_trees;     /* trees per nodal point and time level                    */
+  uint64_t seed;        /* time level k uses seed + k·0x9E3779B97F4A7C15           */
+} rt_pdd_cfg;
+
+/* Nodal point coordinates [6][n_s][2] (host buffer) of the layout above. */
+rt_status rt_pdd_nodes(const rt_pdd_cfg* cfg, double* out_points);
+
+/* Downstream only, stream-ordered on device buffers: d_nodal [6][n_t][n_s]
+ * nodal values → d_field [(n_cells+1)²].  d_bc (may be NULL) receives the
+ * boundary tables [6][n_steps+1][n_cells+1] (spline values at (x_i, t_n)).
+ * RT_E_ARG: bad geometry (see rt_pdd_cfg), dim != 2, a strategy other than
+ * RT_STRATEGY_POTENTIAL or variable coefficients, null pointers. */
+rt_status rt_pdd_downstream_dev(rt_handle* h, const rt_pdd_cfg* cfg, const double* d_nodal,
+                                double* d_field, double* d_bc, void* stream);
+
+/* The whole PDD (synchronous, host buffers): nodal values by the tree walk,
+ * splines, subdomain solves.  out_nodal [6][n_t][n_s] and out_ms[3] = {T_MC,
+ * T_INT, T_LOCAL} (device time, ms) may be NULL. */
+rt_status rt_pdd_solve(rt_handle* h, const rt_pdd_cfg* cfg, double* out_field, double* out_nodal,
+                       double* out_ms);
+
 /* Thread-local message of the last failure on this thread ("" if none). */
 const char* rt_last_error(void);
 

@@ -5,6 +5,6 @@ The product is the C-ABI library ``librt.so`` (include/rt.h); ``rt`` is its
 ctypes binding.  Build with ``python -m paper_2402_06491_b200.build``.
 """
 from . import rt  # noqa: F401
-from .rt import Estimator, finalize, pade, pade_host, philox  # noqa: F401
+from .rt import Estimator, finalize, pade, pade_host, pdd_nodes, philox  # noqa: F401
 
-__all__ = ["rt", "Estimator", "finalize", "pade", "pade_host", "philox"]
+__all__ = ["rt", "Estimator", "finalize", "pade", "pade_host", "pdd_nodes", "philox"]

@@ -1,0 +1,247 @@
+// pdd.cuh — probabilistic domain decomposition downstream (NEXT row f1,
+// DESIGN.md §12): the interface values produced by the tree walk are turned
+// into Dirichlet data and four fully decoupled subdomain solves
+// ("Interpolation" and "Local solver", 1007-1012).
+//
+//   pdd_spline_kernel: one thread per (line, grid node s_i): the tensor-product
+//     not-a-knot cubic spline in (s, t) of that line's nodal table
+//     (PAPER.md:939-942), evaluated at s_i for every time step t_n.
+//   pdd_adi_kernel: one CTA per subdomain (the paper's "each subdomain ...
+//     assigned to different processors" — here an SM each), the whole time
+//     march in shared memory: Strang splitting with RK4 half reactions and a
+//     Peaceman–Rachford ADI diffusion step (Crank–Nicolson per direction,
+//     PAPER.md:971-973), Dirichlet data carried through the same splitting.
+//
+// Geometry (square [lo, hi]^2 split at mid = (lo + hi)/2): grid nodes
+// x_i = lo + i h, i = 0..n, h = (hi - lo)/n, n even, m = n/2 cells per
+// subdomain side.  Lines: 0 interface x = mid (s = y), 1 interface y = mid
+// (s = x), 2 edge x = lo, 3 edge x = hi (s = y), 4 edge y = lo, 5 edge y = hi
+// (s = x).  Nodal table V[line][k][j] at s_j = lo + j (hi - lo)/(ns - 1),
+// t_k = k T/(nt - 1).  Boundary table W[line][step][i] at (s = x_i, t_step).
+#pragma once
+#include <cstdint>
+
+namespace rtk {
+
+constexpr int kPddMaxNodes = 64;    // ns, nt <= 64
+
+// Second derivatives of the not-a-knot cubic spline through y[0..n) on a
+// uniform grid (n >= 4).  With M0 = 2M1 - M2 and M_{n-1} = 2M_{n-2} - M_{n-3}
+// (third derivative continuous at x_1, x_{n-2}) the first and last interior
+// C² equations reduce to 6 M_1 = r_1 and 6 M_{n-2} = r_{n-2}; the rest is the
+// tridiagonal (1, 4, 1) system, r_i = 6 (y_{i+1} - 2 y_i + y_{i-1}) / h².
+__device__ inline void nak_m(const double* y, int n, double h, double* M) {
+  double cp[kPddMaxNodes], dp[kPddMaxNodes];
+  const double s = 6.0 / (h * h);
+  M[1] = (y[2] - 2.0 * y[1] + y[0]) * s / 6.0;
+  M[n - 2] = (y[n - 1] - 2.0 * y[n - 2] + y[n - 3]) * s / 6.0;
+  // interior unknowns M_2..M_{n-3} (Thomas)
+  const int a = 2, b = n - 3;
+  for (int i = a; i <= b; ++i) {
+    double r = (y[i + 1] - 2.0 * y[i] + y[i - 1]) * s;
+    if (i == a) r -= M[1];
+    if (i == b) r -= M[n - 2];
+    const double den = (i == a) ? 4.0 : 4.0 - cp[i - 1];
+    cp[i] = 1.0 / den;
+    dp[i] = (i == a) ? r / den : (r - dp[i - 1]) / den;
+  }
+  for (int i = b; i >= a; --i) M[i] = (i == b) ? dp[i] : dp[i] - cp[i] * M[i + 1];
+  M[0] = 2.0 * M[1] - M[2];
+  M[n - 1] = 2.0 * M[n - 2] - M[n - 3];
+}
+
+__device__ inline double nak_at(const double* y, const double* M, int n, double x0, double h,
+                                double x) {
+  int j = static_cast<int>(floor((x - x0) / h));
+  j = j < 0 ? 0 : (j > n - 2 ? n - 2 : j);
+  const double a = x0 + j * h, b = a + h;
+  return M[j] * (b - x) * (b - x) * (b - x) / (6.0 * h) +
+         M[j + 1] * (x - a) * (x - a) * (x - a) / (6.0 * h) +
+         (y[j] / h - M[j] * h / 6.0) * (b - x) + (y[j + 1] / h - M[j + 1] * h / 6.0) * (x - a);
+}
+
+struct PddGeom {
+  double lo, hi, h, T, dt;
+  int n, m, ns, nt, n_steps;
+};
+
+// W[line][step][i] from V[line][k][j]; one thread per (line, i).
+__global__ void pdd_spline_kernel(const double* __restrict__ V, double* __restrict__ W,
+                                  PddGeom G, int n_lines) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n_lines * (G.n + 1)) return;
+  const int line = q / (G.n + 1), i = q - line * (G.n + 1);
+  const double x = G.lo + i * G.h;
+  const double hs = (G.hi - G.lo) / (G.ns - 1), ht = G.T / (G.nt - 1);
+  double row[kPddMaxNodes], M[kPddMaxNodes], A[kPddMaxNodes], Ma[kPddMaxNodes];
+  const double* Vl = V + static_cast<int64_t>(line) * G.nt * G.ns;
+  for (int k = 0; k < G.nt; ++k) {          // splines in s at every time node
+    for (int j = 0; j < G.ns; ++j) row[j] = Vl[k * G.ns + j];
+    nak_m(row, G.ns, hs, M);
+    A[k] = nak_at(row, M, G.ns, G.lo, hs, x);
+  }
+  nak_m(A, G.nt, ht, Ma);                    // then the spline in t at s = x_i
+  double* Wl = W + static_cast<int64_t>(line) * (G.n_steps + 1) * (G.n + 1) + i;
+  for (int st = 0; st <= G.n_steps; ++st)
+    Wl[static_cast<int64_t>(st) * (G.n + 1)] = nak_at(A, Ma, G.nt, 0.0, ht, st * G.dt);
+}
+
+struct PddEq {
+  double b[9];
+  int degree;
+  int init_kind;
+  double amp, inv_scale, inv_scale2, D;
+};
+
+__device__ inline double pdd_f(const PddEq& E, double u) {
+  double r = E.b[E.degree];
+  for (int k = E.degree - 1; k >= 0; --k) r = fma(r, u, E.b[k]);
+  return r;
+}
+
+__device__ inline double pdd_rk4(const PddEq& E, double u, double hh) {
+  const double k1 = pdd_f(E, u);
+  const double k2 = pdd_f(E, u + 0.5 * hh * k1);
+  const double k3 = pdd_f(E, u + 0.5 * hh * k2);
+  const double k4 = pdd_f(E, u + hh * k3);
+  return u + hh / 6.0 * (k1 + 2.0 * k2 + 2.0 * k3 + k4);
+}
+
+__device__ inline double pdd_g(const PddEq& E, double x, double y) {
+  const double r2 = x * x + y * y;
+  switch (E.init_kind) {
+    case 0: return E.amp;
+    case 1: return E.amp * 0.5 * (1.0 + tanh(x * E.inv_scale));
+    case 2: return E.amp * exp(-r2 * E.inv_scale2);
+    default: return E.amp / (1.0 + r2 * E.inv_scale2);
+  }
+}
+
+// One CTA per subdomain q = qx + 2 qy.  Shared memory: u, u* [(m+1)^2] with
+// index [i][j] = (x_i, y_j) of the subdomain, the four edges' bB and bM
+// [4][m+1], the Thomas factors of (I - r/2 δ²) [m].  Writes its nodes of the
+// global field F[(n+1)^2] (index [i][j] global).
+__global__ void pdd_adi_kernel(const double* __restrict__ W, double* __restrict__ F, PddGeom G,
+                               PddEq E) {
+  extern __shared__ double sm[];
+  const int m = G.m, mm = m + 1;
+  const int qx = blockIdx.x & 1, qy = blockIdx.x >> 1;
+  double* u = sm;                    // [mm][mm]
+  double* us = u + mm * mm;          // [mm][mm]
+  double* eB = us + mm * mm;         // [4][mm] edges: 0 x0, 1 x1, 2 y0, 3 y1
+  double* eM = eB + 4 * mm;          // [4][mm]
+  double* cp = eM + 4 * mm;          // [mm] Thomas: c'_i
+  double* piv = cp + mm;             // [mm] Thomas: 1/(b - a c'_{i-1})
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int i0 = qx * m, j0 = qy * m;             // global offsets
+  // edge lines of this subdomain (see the header)
+  const int lx0 = qx == 0 ? 2 : 0, lx1 = qx == 0 ? 0 : 3;
+  const int ly0 = qy == 0 ? 4 : 1, ly1 = qy == 0 ? 1 : 5;
+  const int64_t lstride = static_cast<int64_t>(G.n_steps + 1) * (G.n + 1);
+  auto Wat = [&](int line, int st, int gi) -> double {
+    return W[line * lstride + static_cast<int64_t>(st) * (G.n + 1) + gi];
+  };
+  const double r = E.D * G.dt / (G.h * G.h);
+  if (tid == 0) {                     // Thomas factors of tridiag(-r/2, 1 + r, -r/2), size m-1
+    for (int k = 1; k <= m - 1; ++k) {
+      const double den = (k == 1) ? 1.0 + r : 1.0 + r - (-0.5 * r) * cp[k - 1];
+      piv[k] = 1.0 / den;
+      cp[k] = (-0.5 * r) * piv[k];
+    }
+  }
+  for (int q = tid; q < mm * mm; q += nth) {      // u(x, y, 0) = g
+    const int i = q / mm, j = q - i * mm;
+    u[q] = pdd_g(E, G.lo + (i0 + i) * G.h, G.lo + (j0 + j) * G.h);
+  }
+  __syncthreads();
+  auto impose = [&](double* w, int st) {           // boundary = W at step st
+    for (int k = tid; k < mm; k += nth) {
+      w[0 * mm + k] = Wat(lx0, st, j0 + k);
+      w[m * mm + k] = Wat(lx1, st, j0 + k);
+    }
+    __syncthreads();
+    for (int k = tid; k < mm; k += nth) {
+      w[k * mm + 0] = Wat(ly0, st, i0 + k);
+      w[k * mm + m] = Wat(ly1, st, i0 + k);
+    }
+    __syncthreads();
+  };
+  impose(u, 0);
+  for (int n = 0; n < G.n_steps; ++n) {
+    for (int q = tid; q < mm * mm; q += nth) u[q] = pdd_rk4(E, u[q], 0.5 * G.dt);   // -> bA
+    __syncthreads();
+    // bB = R_{-dt/2} W(t_{n+1}); bM = (bA + bB)/2, per edge
+    for (int k = tid; k < mm; k += nth) {
+      const double b0 = pdd_rk4(E, Wat(lx0, n + 1, j0 + k), -0.5 * G.dt);
+      const double b1 = pdd_rk4(E, Wat(lx1, n + 1, j0 + k), -0.5 * G.dt);
+      const double b2 = pdd_rk4(E, Wat(ly0, n + 1, i0 + k), -0.5 * G.dt);
+      const double b3 = pdd_rk4(E, Wat(ly1, n + 1, i0 + k), -0.5 * G.dt);
+      eB[0 * mm + k] = b0; eB[1 * mm + k] = b1; eB[2 * mm + k] = b2; eB[3 * mm + k] = b3;
+      eM[0 * mm + k] = 0.5 * (u[0 * mm + k] + b0);
+      eM[1 * mm + k] = 0.5 * (u[m * mm + k] + b1);
+      eM[2 * mm + k] = 0.5 * (u[k * mm + 0] + b2);
+      eM[3 * mm + k] = 0.5 * (u[k * mm + m] + b3);
+    }
+    __syncthreads();
+    // x-sweep: row j (thread), unknowns i = 1..m-1:
+    // (I - r/2 δx²) u* = (I + r/2 δy²) u with u* = bM on the x edges
+    for (int j = 1 + tid; j <= m - 1; j += nth) {
+      double prev = 0.0;
+      for (int i = 1; i <= m - 1; ++i) {
+        double d = u[i * mm + j] + 0.5 * r * (u[i * mm + j - 1] - 2.0 * u[i * mm + j] + u[i * mm + j + 1]);
+        if (i == 1) d += 0.5 * r * eM[0 * mm + j];
+        if (i == m - 1) d += 0.5 * r * eM[1 * mm + j];
+        prev = (i == 1) ? d * piv[i] : (d - (-0.5 * r) * prev) * piv[i];
+        us[i * mm + j] = prev;                      // forward pass: d'_i
+      }
+      for (int i = m - 2; i >= 1; --i) us[i * mm + j] -= cp[i] * us[(i + 1) * mm + j];
+    }
+    for (int k = tid; k < mm; k += nth) {           // u* boundary = bM
+      us[0 * mm + k] = eM[0 * mm + k];
+      us[m * mm + k] = eM[1 * mm + k];
+    }
+    __syncthreads();
+    for (int k = tid; k < mm; k += nth) {
+      us[k * mm + 0] = eM[2 * mm + k];
+      us[k * mm + m] = eM[3 * mm + k];
+    }
+    __syncthreads();
+    // y-sweep: column i (thread), unknowns j = 1..m-1:
+    // (I - r/2 δy²) v = (I + r/2 δx²) u* with v = bB on the y edges
+    for (int i = 1 + tid; i <= m - 1; i += nth) {
+      double prev = 0.0;
+      for (int j = 1; j <= m - 1; ++j) {
+        double d = us[i * mm + j] + 0.5 * r * (us[(i - 1) * mm + j] - 2.0 * us[i * mm + j] + us[(i + 1) * mm + j]);
+        if (j == 1) d += 0.5 * r * eB[2 * mm + i];
+        if (j == m - 1) d += 0.5 * r * eB[3 * mm + i];
+        prev = (j == 1) ? d * piv[j] : (d - (-0.5 * r) * prev) * piv[j];
+        u[i * mm + j] = prev;
+      }
+      for (int j = m - 2; j >= 1; --j) u[i * mm + j] -= cp[j] * u[i * mm + j + 1];
+    }
+    __syncthreads();
+    for (int k = tid; k < mm; k += nth) {           // v boundary = bB
+      u[0 * mm + k] = eB[0 * mm + k];
+      u[m * mm + k] = eB[1 * mm + k];
+    }
+    __syncthreads();
+    for (int k = tid; k < mm; k += nth) {
+      u[k * mm + 0] = eB[2 * mm + k];
+      u[k * mm + m] = eB[3 * mm + k];
+    }
+    __syncthreads();
+    for (int q = tid; q < mm * mm; q += nth) u[q] = pdd_rk4(E, u[q], 0.5 * G.dt);
+    __syncthreads();
+    impose(u, n + 1);
+  }
+  for (int q = tid; q < mm * mm; q += nth) {
+    const int i = q / mm, j = q - i * mm;
+    F[static_cast<int64_t>(i0 + i) * (G.n + 1) + (j0 + j)] = u[q];
+  }
+}
+
+__host__ __device__ constexpr int pdd_smem_bytes(int m) {
+  return (2 * (m + 1) * (m + 1) + 8 * (m + 1) + 2 * (m + 1)) * 8;
+}
+
+}  // namespace rtk

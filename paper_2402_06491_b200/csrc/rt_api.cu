@@ -18,6 +18,7 @@
 #include "../../include/rt.h"
 #include "philox.cuh"
 #include "tree_walk.cuh"
+#include "pdd.cuh"
 
 using rtk::WalkParams;
 
@@ -86,7 +87,7 @@ struct rt_handle {
   cudaStream_t last_stream = nullptr;
   bool have_timing = false;
   double host_total_ms = -1.0;
-  DevBuf partials, gpool, gaux, wtime, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
+  DevBuf partials, gpool, gaux, wtime, pdd_pts, pdd_nodal, pdd_bc, pdd_field, pdd_c, pdd_u, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
   int32_t grid_override = 0;
   int64_t tpt_override = 0;
   int32_t pool_override = 0;
@@ -218,7 +219,8 @@ extern "C" rt_status rt_destroy(rt_handle* h) {
   if (!h) return RT_OK;
   if (h->own_stream) cudaStreamSynchronize(h->own_stream);
   if (h->last_stream) cudaStreamSynchronize(h->last_stream);
-  for (DevBuf* b : {&h->partials, &h->gpool, &h->gaux, &h->wtime, &h->sums, &h->stats, &h->h_points, &h->h_coeffs,
+  for (DevBuf* b : {&h->partials, &h->gpool, &h->gaux, &h->wtime, &h->pdd_pts, &h->pdd_nodal,
+                    &h->pdd_bc, &h->pdd_field, &h->pdd_c, &h->pdd_u, &h->sums, &h->stats, &h->h_points, &h->h_coeffs,
                     &h->h_stderr, &h->h_aux, &h->h_flags})
     b->release();
   for (int q = 0; q < 4; ++q)
@@ -855,5 +857,187 @@ extern "C" rt_status rt_philox_dev(uint64_t key, const uint32_t* d_ctr, int64_t 
   philox_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       rtk::make_round_keys(key), d_ctr, n, d_out);
   RT_CUDA(cudaGetLastError());
+  return RT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// NEXT row f1: PDD downstream (pdd.cuh)
+static rt_status check_pdd(const rt_handle* h, const rt_pdd_cfg* c) {
+  if (!c) return fail(RT_E_ARG, "null cfg");
+  if (h) {
+    if (h->p.dim != 2) return fail(RT_E_ARG, "PDD is implemented for dim = 2");
+    if (h->p.strategy != RT_STRATEGY_POTENTIAL) return fail(RT_E_ARG, "PDD needs RT_STRATEGY_POTENTIAL");
+    for (int k = 0; k <= 8; ++k)
+      if (h->p.coef_kind[k] != RT_COEF_CONST) return fail(RT_E_ARG, "PDD needs constant coefficients");
+  }
+  if (!is_fin(c->lo) || !is_fin(c->hi) || !(c->hi > c->lo)) return fail(RT_E_ARG, "need lo < hi");
+  if (!(c->T > 0.0) || !is_fin(c->T)) return fail(RT_E_ARG, "T must be > 0");
+  if (c->n_cells < 4 || c->n_cells > 1020 || (c->n_cells & 1))
+    return fail(RT_E_ARG, "n_cells must be even in [4, 1020]");
+  if (c->n_steps < 1) return fail(RT_E_ARG, "n_steps must be >= 1");
+  if (c->n_s < 4 || c->n_s > rtk::kPddMaxNodes || c->n_t < 4 || c->n_t > rtk::kPddMaxNodes)
+    return fail(RT_E_ARG, "n_s and n_t must be in [4, %d]", rtk::kPddMaxNodes);
+  if (c->boundary != 0 && c->boundary != 1) return fail(RT_E_ARG, "boundary must be 0 or 1");
+  const int m = c->n_cells / 2;
+  if (rtk::pdd_smem_bytes(m) > 227 * 1024) return fail(RT_E_ARG, "n_cells too large for shared memory");
+  return RT_OK;
+}
+
+static rtk::PddGeom pdd_geom(const rt_pdd_cfg* c) {
+  rtk::PddGeom G;
+  G.lo = c->lo; G.hi = c->hi; G.n = c->n_cells; G.m = c->n_cells / 2;
+  G.h = (c->hi - c->lo) / c->n_cells; G.T = c->T; G.n_steps = c->n_steps;
+  G.dt = c->T / c->n_steps; G.ns = c->n_s; G.nt = c->n_t;
+  return G;
+}
+
+static rtk::PddEq pdd_eq(const rt_eq_params& p) {
+  rtk::PddEq E;
+  for (int k = 0; k < 9; ++k) E.b[k] = (k <= p.degree) ? p.b[k] : 0.0;
+  E.degree = p.degree; E.init_kind = p.init_kind; E.amp = p.init_amp;
+  E.inv_scale = 1.0 / p.init_scale; E.inv_scale2 = 1.0 / (p.init_scale * p.init_scale); E.D = p.D;
+  return E;
+}
+
+extern "C" rt_status rt_pdd_nodes(const rt_pdd_cfg* cfg, double* out) {
+  rt_status s = check_pdd(nullptr, cfg);
+  if (s != RT_OK) return s;
+  if (!out) return fail(RT_E_ARG, "null pointer");
+  const double mid = 0.5 * (cfg->lo + cfg->hi);
+  for (int line = 0; line < 6; ++line)
+    for (int j = 0; j < cfg->n_s; ++j) {
+      const double sj = lin(cfg->lo, cfg->hi, cfg->n_s, j);
+      double x = 0.0, y = 0.0;
+      switch (line) {
+        case 0: x = mid; y = sj; break;
+        case 1: x = sj; y = mid; break;
+        case 2: x = cfg->lo; y = sj; break;
+        case 3: x = cfg->hi; y = sj; break;
+        case 4: x = sj; y = cfg->lo; break;
+        default: x = sj; y = cfg->hi; break;
+      }
+      out[(line * cfg->n_s + j) * 2 + 0] = x;
+      out[(line * cfg->n_s + j) * 2 + 1] = y;
+    }
+  return RT_OK;
+}
+
+static rt_status pdd_downstream(rt_handle* h, const rt_pdd_cfg* cfg, const double* d_nodal,
+                                double* d_field, double* d_bc, cudaStream_t st) {
+  const rtk::PddGeom G = pdd_geom(cfg);
+  double* bc = d_bc;
+  if (!bc) {
+    RT_CUDA(h->pdd_bc.ensure(static_cast<size_t>(6) * (G.n_steps + 1) * (G.n + 1) * sizeof(double)));
+    bc = static_cast<double*>(h->pdd_bc.p);
+  }
+  const int nthr = 6 * (G.n + 1);
+  rtk::pdd_spline_kernel<<<(nthr + 127) / 128, 128, 0, st>>>(d_nodal, bc, G, 6);
+  RT_CUDA(cudaGetLastError());
+  RT_CUDA(cudaEventRecord(h->ev[3], st));
+  const int smem = rtk::pdd_smem_bytes(G.m);
+  RT_CUDA(cudaFuncSetAttribute((const void*)rtk::pdd_adi_kernel,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int threads = std::min(1024, ((G.m + 1 + 31) / 32) * 32);
+  rtk::pdd_adi_kernel<<<4, threads, smem, st>>>(bc, d_field, G, pdd_eq(h->p));
+  RT_CUDA(cudaGetLastError());
+  return RT_OK;
+}
+
+extern "C" rt_status rt_pdd_downstream_dev(rt_handle* h, const rt_pdd_cfg* cfg,
+                                           const double* d_nodal, double* d_field, double* d_bc,
+                                           void* stream) {
+  if (!h) return fail(RT_E_ARG, "null handle");
+  rt_status s = check_pdd(h, cfg);
+  if (s != RT_OK) return s;
+  if (!d_nodal || !d_field) return fail(RT_E_ARG, "null pointer");
+  return pdd_downstream(h, cfg, d_nodal, d_field, d_bc, static_cast<cudaStream_t>(stream));
+}
+
+// t_0 nodal values: g at the nodal points (no Monte Carlo at t = 0)
+__global__ void pdd_init_kernel(const double* __restrict__ pts, double* __restrict__ V, int ns,
+                                int nt, rtk::PddEq E) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= 6 * ns) return;
+  const int line = q / ns, j = q - line * ns;
+  V[(static_cast<int64_t>(line) * nt + 0) * ns + j] = rtk::pdd_g(E, pts[2 * q], pts[2 * q + 1]);
+}
+
+extern "C" rt_status rt_pdd_solve(rt_handle* h, const rt_pdd_cfg* cfg, double* out_field,
+                                  double* out_nodal, double* out_ms) {
+  if (!h) return fail(RT_E_ARG, "null handle");
+  rt_status s = check_pdd(h, cfg);
+  if (s != RT_OK) return s;
+  if (!out_field) return fail(RT_E_ARG, "null pointer");
+  const int K = h->p.K;
+  s = check_pade_args(1, K, cfg->L, cfg->M);
+  if (s != RT_OK) return s;
+  const int ns = cfg->n_s, nt = cfg->n_t, n1 = cfg->n_cells + 1;
+  const int lines_mc = cfg->boundary ? 6 : 2;
+  const int64_t npts = static_cast<int64_t>(lines_mc) * ns;
+  s = check_run_args(h, npts, cfg->T, 0, cfg->n_trees);
+  if (s != RT_OK) return s;
+  cudaStream_t st = h->own_stream;
+  std::vector<double> pts(6 * ns * 2);
+  rt_pdd_nodes(cfg, pts.data());
+  RT_CUDA(h->pdd_pts.ensure(pts.size() * sizeof(double)));
+  RT_CUDA(h->pdd_nodal.ensure(static_cast<size_t>(6) * nt * ns * sizeof(double)));
+  RT_CUDA(h->pdd_field.ensure(static_cast<size_t>(n1) * n1 * sizeof(double)));
+  RT_CUDA(h->pdd_c.ensure(static_cast<size_t>(npts) * (K + 1) * sizeof(double)));
+  RT_CUDA(h->pdd_u.ensure(static_cast<size_t>(npts) * sizeof(double)));
+  RT_CUDA(h->sums.ensure(static_cast<size_t>(npts) * (K + 2) * 3 * sizeof(double)));
+  double* d_pts = static_cast<double*>(h->pdd_pts.p);
+  double* V = static_cast<double*>(h->pdd_nodal.p);
+  double* dc = static_cast<double*>(h->pdd_c.p);
+  double* du = static_cast<double*>(h->pdd_u.p);
+  double* sums = static_cast<double*>(h->sums.p);
+  RT_CUDA(cudaMemcpyAsync(d_pts, pts.data(), pts.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  RT_CUDA(cudaMemsetAsync(V, 0, static_cast<size_t>(6) * nt * ns * sizeof(double), st));
+  cudaEvent_t e0, e1;
+  RT_CUDA(cudaEventCreate(&e0));
+  RT_CUDA(cudaEventCreate(&e1));
+  RT_CUDA(cudaEventRecord(e0, st));
+  pdd_init_kernel<<<(6 * ns + 127) / 128, 128, 0, st>>>(d_pts, V, ns, nt, pdd_eq(h->p));
+  RT_CUDA(cudaGetLastError());
+  // probabilistic part: the interface (and edge) values at
+  // every time level t_k > 0 by the tree walk, resummed by [L/M] Padé
+  for (int k = 1; k < nt; ++k) {
+    const double tk = cfg->T * (static_cast<double>(k) / (nt - 1));
+    const uint64_t seed_k = cfg->seed + static_cast<uint64_t>(k) * 0x9E3779B97F4A7C15ull;
+    s = run_walk(h, d_pts, npts, tk, 0, cfg->n_trees, seed_k, 0, nullptr, sums, st);
+    if (s != RT_OK) return s;
+    finalize_kernel<<<static_cast<unsigned>(npts), 32, 0, st>>>(
+        sums, K, static_cast<double>(cfg->n_trees), dc, nullptr, nullptr, nullptr);
+    pade_kernel<<<static_cast<unsigned>((npts + 127) / 128), 128, 0, st>>>(dc, npts, K + 1, cfg->L,
+                                                                          cfg->M, du, nullptr);
+    RT_CUDA(cudaGetLastError());
+    // du [line][j] -> V[line][k][j]
+    RT_CUDA(cudaMemcpy2DAsync(V + static_cast<size_t>(k) * ns, static_cast<size_t>(nt) * ns * 8, du,
+                              static_cast<size_t>(ns) * 8, static_cast<size_t>(ns) * 8, lines_mc,
+                              cudaMemcpyDeviceToDevice, st));
+  }
+  RT_CUDA(cudaEventRecord(e1, st));
+  // outer edges with zero Dirichlet data: lines 2..5 stay 0 at every level
+  if (!cfg->boundary)
+    RT_CUDA(cudaMemsetAsync(V + static_cast<size_t>(2) * nt * ns, 0,
+                            static_cast<size_t>(4) * nt * ns * sizeof(double), st));
+  double* F = static_cast<double*>(h->pdd_field.p);
+  s = pdd_downstream(h, cfg, V, F, nullptr, st);
+  if (s != RT_OK) return s;
+  RT_CUDA(cudaEventRecord(h->ev[2], st));
+  RT_CUDA(cudaMemcpyAsync(out_field, F, static_cast<size_t>(n1) * n1 * sizeof(double),
+                          cudaMemcpyDeviceToHost, st));
+  if (out_nodal)
+    RT_CUDA(cudaMemcpyAsync(out_nodal, V, static_cast<size_t>(6) * nt * ns * sizeof(double),
+                            cudaMemcpyDeviceToHost, st));
+  RT_CUDA(cudaStreamSynchronize(st));
+  if (out_ms) {
+    float a = 0.f, b = 0.f, c = 0.f;
+    RT_CUDA(cudaEventElapsedTime(&a, e0, e1));
+    RT_CUDA(cudaEventElapsedTime(&b, e1, h->ev[3]));
+    RT_CUDA(cudaEventElapsedTime(&c, h->ev[3], h->ev[2]));
+    out_ms[0] = a; out_ms[1] = b; out_ms[2] = c;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   return RT_OK;
 }

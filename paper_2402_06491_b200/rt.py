@@ -24,7 +24,8 @@ PREC_FP64, PREC_FP32_POS = 0, 1
 # every symbol include/rt.h declares
 SYMBOLS = ("rt_create", "rt_destroy", "rt_estimate", "rt_estimate_dev", "rt_sums_dev",
            "rt_finalize_dev", "rt_pade", "rt_pade_dev", "rt_interface_values", "rt_trace_dev",
-           "rt_get_stats", "rt_set_launch", "rt_set_pool", "rt_philox_dev", "rt_last_error")
+           "rt_get_stats", "rt_set_launch", "rt_set_pool", "rt_philox_dev", "rt_last_error",
+           "rt_pdd_nodes", "rt_pdd_downstream_dev", "rt_pdd_solve")
 
 
 class RTError(RuntimeError):
@@ -40,6 +41,20 @@ class EqParams(C.Structure):
                 ("K", C.c_int32), ("precision", C.c_int32),
                 ("strategy", C.c_int32), ("q", C.c_double), ("coef_kind", C.c_int32 * 9),
                 ("coef_axis", C.c_int32), ("coef_scale", C.c_double), ("coef_t0", C.c_double)]
+
+
+class PddCfg(C.Structure):
+    _fields_ = [("lo", C.c_double), ("hi", C.c_double), ("T", C.c_double), ("n_cells", C.c_int32),
+                ("n_steps", C.c_int32), ("n_s", C.c_int32), ("n_t", C.c_int32),
+                ("boundary", C.c_int32), ("L", C.c_int32), ("M", C.c_int32),
+                ("n_trees", C.c_int64), ("seed", C.c_uint64)]
+
+
+def pdd_cfg(c: dict) -> PddCfg:
+    p = PddCfg()
+    for k, _ in PddCfg._fields_:
+        setattr(p, k, c[k])
+    return p
 
 
 class Stats(C.Structure):
@@ -83,6 +98,9 @@ def lib():
             "rt_get_stats": ([H, C.POINTER(Stats)]),
             "rt_set_launch": ([H, i32, i64]),
             "rt_set_pool": ([H, i32]),
+            "rt_pdd_nodes": ([C.POINTER(PddCfg), dp]),
+            "rt_pdd_downstream_dev": ([H, C.POINTER(PddCfg), dp, dp, dp, vp]),
+            "rt_pdd_solve": ([H, C.POINTER(PddCfg), dp, dp, dp]),
             "rt_philox_dev": ([u64, vp, i64, vp, vp]),
         }
         for name, args in sig.items():
@@ -177,6 +195,30 @@ class Estimator:
         """Cap the per-warp shared-memory stack pool (0 = automatic); smaller
         pools push more stack entries to the global overflow area (tests)."""
         _check(lib().rt_set_pool(self._h, entries))
+
+    # -- NEXT row f1: probabilistic domain decomposition (rt_pdd_*) ----------
+    def pdd_solve(self, cfg: dict):
+        """rt_pdd_solve: the whole PDD on host buffers.  Returns (field
+        [(n+1), (n+1)], nodal values [6, n_t, n_s], {T_MC, T_INT, T_LOCAL} ms)."""
+        n1 = cfg["n_cells"] + 1
+        F = np.empty((n1, n1))
+        V = np.empty((6, cfg["n_t"], cfg["n_s"]))
+        ms = np.empty(3)
+        _check(lib().rt_pdd_solve(self._h, C.byref(pdd_cfg(cfg)), _ptr(F), _ptr(V), _ptr(ms)))
+        return F, V, dict(T_MC=float(ms[0]), T_INT=float(ms[1]), T_LOCAL=float(ms[2]))
+
+    def pdd_downstream(self, cfg: dict, nodal, want_bc: bool = False, stream=None):
+        """rt_pdd_downstream_dev on a CUDA tensor nodal [6, n_t, n_s]: returns
+        (field [(n+1), (n+1)], boundary tables [6, n_steps+1, n+1] or None)."""
+        import torch
+        V = _dev_f64(nodal, cfg["n_s"]).reshape(6, cfg["n_t"], cfg["n_s"])
+        n1 = cfg["n_cells"] + 1
+        F = torch.empty((n1, n1), dtype=torch.float64, device=V.device)
+        bc = torch.empty((6, cfg["n_steps"] + 1, n1), dtype=torch.float64, device=V.device) \
+            if want_bc else None
+        _check(lib().rt_pdd_downstream_dev(self._h, C.byref(pdd_cfg(cfg)), _ptr(V), _ptr(F), _ptr(bc),
+                                           _stream(stream)))
+        return F, bc
 
     # -- device API ---------------------------------------------------------
     def estimate(self, points, t: float, n_trees: int, seed: int, stream=None):
@@ -300,4 +342,11 @@ def philox(key: int, ctr):
     c = ctr.contiguous()
     out = torch.empty_like(c)
     _check(lib().rt_philox_dev(int(key), _ptr(c), c.shape[0], _ptr(out), _stream()))
+    return out
+
+
+def pdd_nodes(cfg: dict) -> np.ndarray:
+    """rt_pdd_nodes: nodal point coordinates [6, n_s, 2] of the PDD lines."""
+    out = np.empty((6, cfg["n_s"], 2))
+    _check(lib().rt_pdd_nodes(C.byref(pdd_cfg(cfg)), _ptr(out)))
     return out
