@@ -35,7 +35,8 @@ class Params(C.Structure):
                 ("init_kind", C.c_int32), ("init_amp", C.c_double),
                 ("init_scale", C.c_double), ("K", C.c_int32), ("precision", C.c_int32),
                 ("strategy", C.c_int32), ("q", C.c_double), ("coef_kind", C.c_int32 * 9),
-                ("coef_axis", C.c_int32), ("coef_scale", C.c_double), ("coef_t0", C.c_double)]
+                ("coef_axis", C.c_int32), ("coef_scale", C.c_double), ("coef_t0", C.c_double),
+                ("shared", C.c_int32)]
 
 
 class Norm(C.Structure):
@@ -104,6 +105,7 @@ def params(eq: dict) -> Params:
         p.coef_kind[k] = ck[k]
     p.coef_axis = eq.get("coef_axis", 0); p.coef_scale = eq.get("coef_scale", 1.0)
     p.coef_t0 = eq.get("coef_t0", 0.1)
+    p.shared = eq.get("shared", 0)
     return p
 
 

@@ -89,6 +89,11 @@ int or_normalize(const or_params* p, or_norm* o) {
     if (k == 1 && p->strategy == 0) o->a[k] += lam;
     if (p->coef_kind[k] != 0 && p->coef_kind[k] != 1) return 4;
   }
+  /* shared trees (f4) need node-independent weights: constant coefficients */
+  if (p->shared != 0 && p->shared != 1) return 6;
+  if (p->shared)
+    for (int k = 0; k <= 8; ++k)
+      if (p->coef_kind[k] != 0) return 6;
   /* a variable coefficient cannot ride on the potential's k = 1 term */
   if (p->strategy == 0 && p->coef_kind[1] != 0) return 4;
   for (int k = 0; k <= 8; ++k)
@@ -176,6 +181,7 @@ typedef struct {
   int64_t i, j;
   int32_t ne, leaves, particles;
   int stop;          /* 1 pruned (Ne > K), 2 killed (empty support) */
+  const double* node;  /* shared trees (f4): the node x_i, the walk carries δ */
 } tree_ctx;
 
 /* Value of the sub-tree rooted at the particle with ancestry label `label`
@@ -245,7 +251,14 @@ static double particle(tree_ctx* c, const double* y, double tau, uint64_t label)
 
   if (is_leaf) {                       /* the branch reaches the horizon */
     c->leaves++;
-    double gv = g_eval(p, x);          /* g at the leaf */
+    double gv;
+    if (c->node) {                     /* shared trees: g(x_i + δ) */
+      double xe[3];
+      for (int k = 0; k < p->dim; ++k) xe[k] = c->node[k] + x[k];
+      gv = g_eval(p, xe);
+    } else {
+      gv = g_eval(p, x);               /* g at the leaf */
+    }
     return strat_b ? gv / nz->q_hat : gv;   /* g̃ = g / q */
   }
   /* splitting event */
@@ -271,6 +284,8 @@ static double particle(tree_ctx* c, const double* y, double tau, uint64_t label)
   return val;
 }
 
+static const double ZERO3[3] = {0.0, 0.0, 0.0};
+
 /* Root factor: Strategy A's shift estimates v, and u = v e^{λt}. */
 static double root_factor(const or_params* p, const or_norm* nz, double t) {
   return p->strategy == 1 ? exp(nz->lambda * t) : 1.0;
@@ -281,8 +296,8 @@ int or_tree(const or_params* p, const double* x, int64_t i, int64_t j, double t,
   or_norm nz;
   int e = or_normalize(p, &nz);
   if (e) return e;
-  tree_ctx c = {p, &nz, seed, i, j, 0, 0, 0, 0};
-  double C = root_factor(p, &nz, t) * particle(&c, x, t, 1u);
+  tree_ctx c = {p, &nz, seed, p->shared ? 0 : i, j, 0, 0, 0, 0, p->shared ? x : NULL};
+  double C = root_factor(p, &nz, t) * particle(&c, p->shared ? ZERO3 : x, t, 1u);
   rec->ne = c.ne;
   rec->leaves = c.leaves;
   rec->particles = c.particles;
@@ -298,8 +313,9 @@ int or_trees(const or_params* p, const double* points, int64_t n_points, double 
   if (e) return e;
   for (int64_t i = 0; i < n_points; ++i)
     for (int64_t q = 0; q < n_trees; ++q) {
-      tree_ctx c = {p, &nz, seed, i, j0 + q, 0, 0, 0, 0};
-      double C = root_factor(p, &nz, t) * particle(&c, points + i * p->dim, t, 1u);
+      tree_ctx c = {p, &nz, seed, p->shared ? 0 : i, j0 + q, 0, 0, 0, 0,
+                    p->shared ? points + i * p->dim : NULL};
+      double C = root_factor(p, &nz, t) * particle(&c, p->shared ? ZERO3 : points + i * p->dim, t, 1u);
       or_tree_rec* r = rec + i * n_trees + q;
       r->ne = c.ne; r->leaves = c.leaves; r->particles = c.particles;
       r->pruned = (c.stop == 1);
@@ -317,8 +333,9 @@ int or_trees_at(const or_params* p, const double* points, int64_t n_points, doub
   if (e) return e;
   for (int64_t i = 0; i < n_points; ++i)
     for (int64_t q = 0; q < n_js; ++q) {
-      tree_ctx c = {p, &nz, seed, i, js[q], 0, 0, 0, 0};
-      double C = root_factor(p, &nz, t) * particle(&c, points + i * p->dim, t, 1u);
+      tree_ctx c = {p, &nz, seed, p->shared ? 0 : i, js[q], 0, 0, 0, 0,
+                    p->shared ? points + i * p->dim : NULL};
+      double C = root_factor(p, &nz, t) * particle(&c, p->shared ? ZERO3 : points + i * p->dim, t, 1u);
       or_tree_rec* r = rec + i * n_js + q;
       r->ne = c.ne; r->leaves = c.leaves; r->particles = c.particles;
       r->pruned = (c.stop == 1);
@@ -342,8 +359,9 @@ int or_sums(const or_params* p, const double* points, int64_t n_points, double t
   for (int64_t i = 0; i < n_points; ++i) {
     double* row = sums + i * nb * 3;
     for (int64_t q = 0; q < n_trees; ++q) {
-      tree_ctx c = {p, &nz, seed, i, j0 + q, 0, 0, 0, 0};
-      double C = root_factor(p, &nz, t) * particle(&c, points + i * p->dim, t, 1u);
+      tree_ctx c = {p, &nz, seed, p->shared ? 0 : i, j0 + q, 0, 0, 0, 0,
+                    p->shared ? points + i * p->dim : NULL};
+      double C = root_factor(p, &nz, t) * particle(&c, p->shared ? ZERO3 : points + i * p->dim, t, 1u);
       s.trees++;
       s.particles += c.particles;
       s.leaves += c.leaves;

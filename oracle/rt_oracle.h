@@ -42,6 +42,10 @@ typedef struct {
   int32_t coef_axis;    /* a */
   double  coef_scale;   /* s > 0 */
   double  coef_t0;      /* t0 > 0 */
+  int32_t shared;       /* 1: shared trees (NEXT row f4): the random numbers omit
+                           the node index, every node sees the same trees, node
+                           i's leaves are evaluated at x_i + δ (δ the leaf's
+                           displacement from the root); constant coefficients */
 } or_params;
 
 typedef struct {

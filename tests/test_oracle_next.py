@@ -158,3 +158,59 @@ def test_invalid_strategy_parameters(orc):
                dict(strategy=W.STRAT_A_SHIFT, coef_kind=[0, 0, 1], coef_t0=0.0)):
         with pytest.raises(ValueError):
             orc.normalize(_eq((0.0, 0.0, -1.0), **kw))
+
+
+# ---------------------------------------------------------------------------
+# NEXT row f4: shared trees (common random numbers across nodes)
+def test_shared_trees_structure_is_node_independent(orc):
+    """Every node sees the same trees: structure records identical across
+    nodes, and with constant data identical contributions."""
+    eq = W._eq(1, W.B_CFG2, W.G_CONST, 0.4, 1.0, K=12, shared=1)
+    pts = np.array([[-2.0], [0.0], [0.3], [2.5]])
+    rec = orc.trees(eq, pts, 1.0, 3_000, seed=4)
+    for f in ("ne", "leaves", "particles", "pruned"):
+        assert np.all(rec[f] == rec[f][0:1]), f
+    assert np.all(rec["C"] == rec["C"][0:1])
+
+
+def test_shared_trees_translation(orc):
+    """For a tree with one leaf (Ne = 0) C_i = g(x_i + δ): with Gaussian data
+    log C_i = log A - (x_i + δ)^2, so δ recovered from two nodes predicts C at a
+    third (the leaves are evaluated at x_i + a common displacement)."""
+    eq = W._eq(1, (0.0, -1.0, 0.5), W.G_GAUSS, 1.0, 1.0, K=12, shared=1)
+    pts = np.array([[0.0], [1.0], [-0.7]])
+    rec = orc.trees(eq, pts, 0.6, 2_000, seed=9)
+    one = rec["ne"][0] == 0
+    c0, c1, c2 = (rec["C"][i][one] for i in range(3))
+    # -(x+δ)^2: log c0 - log c1 = (1+δ)^2 - δ^2 = 1 + 2δ
+    delta = (np.log(c0) - np.log(c1) - 1.0) / 2.0
+    assert np.allclose(np.log(c2), -(-0.7 + delta) ** 2, rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("strategy", [W.STRAT_POTENTIAL, W.STRAT_A_SHIFT, W.STRAT_B])
+def test_shared_trees_same_law(orc, strategy):
+    """Per node the estimator is unchanged in law: shared-tree estimates of the
+    Example-1 equation agree with finite differences within 4 s.e."""
+    b, kind, amp, scale, t = EXAMPLES["ex1"]
+    xs = np.array([-1.0, 0.0, 0.8])
+    eq = _eq(b, strategy, kind, amp, scale, K=14, q=0.6, shared=1,
+             lam=1.0 if strategy == W.STRAT_POTENTIAL else 0.0)
+    _, _, us, ses, _ = orc.estimate(eq, xs[:, None], t, 40_000, seed=6)
+    ref = _fd(b, _g(kind, amp, scale), t, xs)
+    assert np.all(np.abs(us - ref) < Z * ses), (us, ref)
+
+
+def test_shared_trees_heat_kernel_2d(orc):
+    """Linear f = -u (no offspring): c_0(x) = e^{-t} E g(x + sqrt(2t) Z) is the
+    heat kernel at every node, d = 2."""
+    import closed_forms as cfm
+    eq = W._eq(2, (0.0, -1.0), W.G_GAUSS, 0.4, 1.0, K=4, shared=1)
+    pts = np.array([[0.0, 0.0], [0.5, -0.4], [1.2, 0.3]])
+    c, se, *_ = orc.estimate(eq, pts, 1.0, 100_000, seed=12)
+    ref = cfm.heat(pts, 1.0, 1.0, 1.0, 0.4)
+    assert np.all(np.abs(c[:, 0] - ref) < Z * se[:, 0]), (c[:, 0], ref)
+
+
+def test_shared_rejects_variable_coefficients(orc):
+    with pytest.raises(ValueError):
+        orc.normalize(_eq((0.0, 0.0, -1.0), W.STRAT_A_SHIFT, shared=1, coef_kind=[0, 0, 1]))

@@ -78,18 +78,20 @@ COEF_CONST, COEF_GAUSS_RATIONAL = 0, 1
 
 def _eq(dim, b, g_kind, g_amp, g_scale, K, D=1.0, lam=0.0,
         offspring=OFFSPRING_ABS, precision=PREC_FP64, strategy=STRAT_POTENTIAL, q=0.5,
-        coef_kind=None, coef_axis=0, coef_scale=1.0, coef_t0=0.1) -> dict:
+        coef_kind=None, coef_axis=0, coef_scale=1.0, coef_t0=0.1, shared=0) -> dict:
     """Equation parameters (the fields of rt_eq_params / or_params).
 
     strategy: 0 exponential clock with potential -λu; 1 Strategy A with the
     shift u = v e^{λt}; 2 Strategy B (q = P(leaf)).  coef_kind[k] = 1 makes the
-    coefficient of u^k variable: b_k exp(-x_a²/s²)/(t + t0) (Example 5)."""
+    coefficient of u^k variable: b_k exp(-x_a²/s²)/(t + t0) (Example 5).
+    shared = 1: every node sees the same trees (NEXT row f4)."""
     bb = list(b) + [0.0] * (9 - len(b))
     ck = list(coef_kind) + [0] * (9 - len(coef_kind)) if coef_kind else [0] * 9
     return dict(dim=dim, D=D, degree=len(b) - 1, b=bb, lam=lam,
                 offspring=offspring, init_kind=g_kind, init_amp=g_amp,
                 init_scale=g_scale, K=K, precision=precision, strategy=strategy, q=q,
-                coef_kind=ck, coef_axis=coef_axis, coef_scale=coef_scale, coef_t0=coef_t0)
+                coef_kind=ck, coef_axis=coef_axis, coef_scale=coef_scale, coef_t0=coef_t0,
+                shared=shared)
 
 
 # BASELINE.json "configs" (SURVEY.md §8(d) table).  b = (b_0, b_1, ...) with
