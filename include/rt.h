@@ -106,6 +106,10 @@ typedef struct {
   int32_t coef_axis;    /* a: the coordinate of the variable factor                */
   double  coef_scale;   /* s > 0                                                   */
   double  coef_t0;      /* t0 > 0                                                  */
+  int32_t shared;       /* 1: shared trees (NEXT row f4): the random  */
+                        /* numbers omit the node index, every node sees the same   */
+                        /* trees, leaves evaluated at x_i + δ; unbiased per node,  */
+                        /* correlated across nodes; constant coefficients, FP64    */
 } rt_eq_params;
 
 typedef struct {
@@ -146,7 +150,8 @@ typedef struct rt_handle rt_handle;
  * an unknown precision, RT_STRATEGY_B with q ∉ (0,1) (or a zero-width integer
  * threshold), a variable coefficient with s <= 0, t0 <= 0, an axis outside
  * [0, dim), or on k = 1 under RT_STRATEGY_POTENTIAL, RT_PREC_FP32_POS with a
- * strategy other than RT_STRATEGY_POTENTIAL.  An empty support (purely linear f) is legal. */
+ * strategy other than RT_STRATEGY_POTENTIAL, shared ∉ {0, 1}, shared trees
+ * with variable coefficients or RT_PREC_FP32_POS.  An empty support (purely linear f) is legal. */
 rt_status rt_create(const rt_eq_params* params, rt_handle** out);
 
 /* Free the handle and its device scratch.  NULL is a no-op. */

@@ -183,6 +183,9 @@ extern "C" rt_status rt_create(const rt_eq_params* params, rt_handle** out) {
     return fail(RT_E_ARG, "unknown strategy %d", p.strategy);
   if (p.precision == RT_PREC_FP32_POS && p.strategy != RT_STRATEGY_POTENTIAL)
     return fail(RT_E_ARG, "the FP32-position variant exists for RT_STRATEGY_POTENTIAL only");
+  if (p.shared != 0 && p.shared != 1) return fail(RT_E_ARG, "shared must be 0 or 1");
+  if (p.shared && p.precision != RT_PREC_FP64)
+    return fail(RT_E_ARG, "shared trees are implemented in FP64 only");
   bool any_var = false;
   for (int k = 0; k <= 8; ++k) {
     if (p.coef_kind[k] != RT_COEF_CONST && p.coef_kind[k] != RT_COEF_GAUSS_RATIONAL)
@@ -190,6 +193,7 @@ extern "C" rt_status rt_create(const rt_eq_params* params, rt_handle** out) {
     any_var = any_var || p.coef_kind[k] == RT_COEF_GAUSS_RATIONAL;
   }
   if (any_var) {
+    if (p.shared) return fail(RT_E_ARG, "shared trees need constant coefficients");
     if (p.strategy == RT_STRATEGY_POTENTIAL && p.coef_kind[1] != RT_COEF_CONST)
       return fail(RT_E_ARG, "a variable coefficient on k = 1 needs a strategy without the potential");
     if (!(p.coef_scale > 0.0) || !is_fin(p.coef_scale) || !(p.coef_t0 > 0.0) ||
@@ -249,19 +253,27 @@ extern "C" rt_status rt_set_pool(rt_handle* h, int32_t pool_entries) {
 // tree-walk launch (rows a3–a7)
 using KernelFn = void (*)(WalkParams);
 
-template <int DIM, int GK, bool REC, bool F32, bool SB>
+template <int DIM, int GK, bool REC, bool F32, bool SB, bool SH = false>
 static KernelFn pick_kernel() {
-  return rtk::tree_walk_kernel<DIM, GK, REC, F32, SB>;
+  return rtk::tree_walk_kernel<DIM, GK, REC, F32, SB, SH>;
 }
 
 // The kernel for (dim, g, rec) and the production (rec = false) kernel whose
 // occupancy fixes the launch geometry for both.
-static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, bool sb, KernelFn* prod,
-                           int* smem, int* pool_cap) {
+static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, bool sb, bool sh, int nb,
+                           KernelFn* prod, int* smem, int* pool_cap) {
 #define RT_K(D, G)                                                              \
   if (dim == D && gk == G) {                                                    \
-    *smem = rtk::smem_bytes<D>();                                               \
+    *smem = rtk::smem_bytes_sh<D>(sh, nb);                                      \
     *pool_cap = rtk::PoolCap<D>::v;                                             \
+    if (sh && sb) {                                                             \
+      *prod = pick_kernel<D, G, false, false, true, true>();                    \
+      return rec ? pick_kernel<D, G, true, false, true, true>() : *prod;        \
+    }                                                                           \
+    if (sh) {                                                                   \
+      *prod = pick_kernel<D, G, false, false, false, true>();                   \
+      return rec ? pick_kernel<D, G, true, false, false, true>() : *prod;       \
+    }                                                                           \
     if (sb) {                                                                   \
       *prod = pick_kernel<D, G, false, false, true>();                          \
       return rec ? pick_kernel<D, G, true, false, true>() : *prod;              \
@@ -404,19 +416,23 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   const Norm& nz = h->nz;
   int smem = 0, pool_cap = 0;
   KernelFn prod = nullptr;
+  const bool sh = p.shared != 0;
   KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, p.precision == RT_PREC_FP32_POS,
-                           p.strategy == RT_STRATEGY_B, &prod, &smem, &pool_cap);
+                           p.strategy == RT_STRATEGY_B, sh, p.K + 2, &prod, &smem, &pool_cap);
   if (!fn) return fail(RT_E_ARG, "no kernel for dim=%d init_kind=%d", p.dim, p.init_kind);
   if (smem > 48 * 1024) {
     RT_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     RT_CUDA(cudaFuncSetAttribute((const void*)prod, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   }
   Launch L;
-  rt_status s = plan_launch(h, prod, smem, n_points, n_trees, L);   // same grid for the trace
+  // shared trees: a task is (32-node tile, tree range)
+  const int64_t n_units = sh ? (n_points + 31) / 32 : n_points;
+  rt_status s = plan_launch(h, prod, smem, n_units, n_trees, L);   // same grid for the trace
   if (s != RT_OK) return s;
   const int nb = p.K + 2;
   const int nf = p.dim + 2;
-  RT_CUDA(h->partials.ensure(static_cast<size_t>(L.n_tasks) * nb * 3 * sizeof(double)));
+  // partials are per node in either mode: [n_points][tpn][nb][3]
+  RT_CUDA(h->partials.ensure(static_cast<size_t>(n_points) * L.tpn * nb * 3 * sizeof(double)));
   // overflow stack entries once a warp's shared-memory pool is exhausted: a
   // lane's stack never exceeds K groups, so 32 (K+1) entries per warp always
   // suffice: [warps][gcap][nf] doubles and [warps][2][gcap] int32
@@ -454,6 +470,7 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   P.coef_t0 = p.coef_t0;
   P.tq = nz.tq;
   P.inv_q = p.strategy == RT_STRATEGY_B ? 1.0 / nz.q_hat : 1.0;
+  P.n_points = static_cast<int32_t>(n_points);
   P.beta = nz.beta;
   P.K = p.K;
   P.nb = nb;

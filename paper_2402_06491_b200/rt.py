@@ -40,7 +40,8 @@ class EqParams(C.Structure):
                 ("init_kind", C.c_int32), ("init_amp", C.c_double), ("init_scale", C.c_double),
                 ("K", C.c_int32), ("precision", C.c_int32),
                 ("strategy", C.c_int32), ("q", C.c_double), ("coef_kind", C.c_int32 * 9),
-                ("coef_axis", C.c_int32), ("coef_scale", C.c_double), ("coef_t0", C.c_double)]
+                ("coef_axis", C.c_int32), ("coef_scale", C.c_double), ("coef_t0", C.c_double),
+                ("shared", C.c_int32)]
 
 
 class PddCfg(C.Structure):
@@ -162,6 +163,7 @@ def eq_params(eq: dict) -> EqParams:
     p.coef_axis = eq.get("coef_axis", 0)
     p.coef_scale = eq.get("coef_scale", 1.0)
     p.coef_t0 = eq.get("coef_t0", 0.1)
+    p.shared = eq.get("shared", 0)
     return p
 
 

@@ -63,6 +63,8 @@ def _create(rtmod, **kw):
     (dict(coef_kind=[0, 1] + [0] * 7), "k = 1"), (dict(coef_kind=[0, 0, 2] + [0] * 6), "coef_kind"),
     (dict(coef_kind=[0, 0, 1] + [0] * 6, coef_t0=0.0), "t0 > 0"),
     (dict(coef_kind=[0, 0, 1] + [0] * 6, coef_axis=1), "axis"),
+    (dict(shared=2), "shared"), (dict(shared=1, precision=1), "FP64"),
+    (dict(shared=1, strategy=1, coef_kind=[0, 0, 1] + [0] * 6), "constant coefficients"),
 ])
 def test_create_rejects(rtmod, kw, frag):
     st, msg = _create(rtmod, **kw)

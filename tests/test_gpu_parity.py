@@ -133,6 +133,15 @@ def _eq_variants():
                                q=0.7, offspring=W.OFFSPRING_UNIFORM), W.random_nodes(6, 2, 13), 0.5, 1_500),
         "pot_var": (dict(base2, coef_kind=[0, 0, 1, 0, 1, 0, 0, 0, 0], coef_axis=0, coef_scale=2.0, coef_t0=0.3),
                     W.random_nodes(6, 1, 14), 1.0, 2_000),
+        # NEXT row f4: shared trees (one tile and ragged second tiles)
+        "sh_cfg2": (dict(base2, shared=1), W.random_nodes(40, 1, 15), 1.0, 1_500),
+        "sh_cfg4": (dict(W.get("cfg4")["eq"], shared=1), W.nodes(W.get("cfg4"))[:64], 1.0, 80),
+        "sh_ex1B": (W._eq(1, (0.0, 0.0, -1.0), W.G_GAUSS, GN, 2.0, K=12, strategy=W.STRAT_B, q=0.6, shared=1),
+                    W.random_nodes(8, 1, 16), 0.5, 3_000),
+        "sh_d3_shift": (W._eq(3, (0.1, -0.5, -1.0, 0.3), W.G_LORENTZ, 0.5, 1.0, K=10,
+                              strategy=W.STRAT_A_SHIFT, lam=1.3, shared=1), W.random_nodes(35, 3, 17), 0.8, 500),
+        "sh_d2_tanh": (dict(W.get("cfg3")["eq"], init_kind=W.G_TANH_STEP, init_amp=1.0, shared=1),
+                       W.random_nodes(33, 2, 18), 0.5, 800),
     }
 
 
@@ -160,7 +169,7 @@ def test_tree_parity(P, orc, name):
 
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg2_uniform", "poisson_k1",
-                                  "shift_ex5_d2", "B_ex3", "B_d3_var"])
+                                  "shift_ex5_d2", "B_ex3", "B_d3_var", "sh_cfg2", "sh_d3_shift"])
 def test_estimate_parity(P, orc, name):
     eq, pts, t, N = CASES[name]
     N = max(N, 2)
@@ -216,7 +225,7 @@ def test_geometry_and_determinism(P):
 
 
 @pytest.mark.parametrize("name,pool", [("cfg4", 1), ("cfg4", 9), ("cfg2_t2", 3), ("d3_gauss", 40),
-                                       ("B_d3_var", 2)])
+                                       ("B_d3_var", 2), ("sh_cfg4", 5)])
 def test_stack_pool_overflow(P, orc, name, pool):
     """A small shared-memory stack pool pushes pending sibling groups to the
     global overflow area; trees must still equal the oracle's, and the sums

@@ -20,7 +20,8 @@ import bench  # noqa: E402
 import paper_2402_06491_b200 as P  # noqa: E402
 import workloads as W  # noqa: E402
 
-NAMES = ("ex1A", "ex1B", "ex3A", "ex3B", "ex5A", "ex5B", "cfg2", "cfg3")
+NAMES = ("ex1A", "ex1B", "ex3A", "ex3B", "ex5A", "ex5B", "cfg2", "cfg3", "cfg4",
+         "cfg2_sh", "cfg3_sh", "cfg4_sh")
 
 
 def main():
@@ -43,15 +44,23 @@ def main():
             st = est.stats()
             ms.append(st["kernel_ms"])
         kms = min(ms)
+        st_ops = dict(st)
+        if eq.get("shared"):
+            # shared trees: each 32-node tile walks the trees once; every node
+            # evaluates g at every leaf (stats count per node-tree)
+            tiles = (n + 31) // 32
+            for k in ("particles", "splits", "trees"):
+                st_ops[k] = st[k] * tiles / n
         c, se = est.estimate(x, t, N, cfg["seed"])
         u, fl = P.pade(c, cfg["L"], cfg["M"])
-        r = dict(workload=name, strategy=["potential", "A_shift", "B"][eq.get("strategy", 0)],
+        r = dict(workload=name, strategy=["potential", "A_shift", "B"][eq.get("strategy", 0)]
+                 + (" shared" if eq.get("shared") else ""),
                  q=eq.get("q") if eq.get("strategy", 0) == 2 else None, dim=eq["dim"], nodes=n,
                  trees_per_node=N, t=t, kernel_ms=kms, trees_per_s=n * N / (kms / 1e3),
                  leaf_evals_per_s=st["leaves"] / (kms / 1e3),
                  particles_per_tree=st["particles"] / st["trees"],
                  pruned_fraction=st["pruned"] / st["trees"],
-                 fp64_roofline_frac=bench.algo_fp64_ops(eq, st) / (kms / 1e3) / peak,
+                 fp64_roofline_frac=bench.algo_fp64_ops(eq, st_ops) / (kms / 1e3) / peak,
                  u_mid=float(u[n // 2].item()))
         rows.append(r)
         print(json.dumps(r), flush=True)

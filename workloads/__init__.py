@@ -143,6 +143,13 @@ for _s, _tag in ((STRAT_A_SHIFT, "A"), (STRAT_B, "B")):
                                 t=0.5, nodes=dict(kind="planes", planes=_CFG3_PLANES, max_points=256),
                                 n_trees=1_000_000, seed=0, L=5, M=5)
 
+# NEXT row f4: the BASELINE configs with shared trees (every node sees the
+# same trees) — a different sampling contract, same per-node law.
+for _n in ("cfg2", "cfg3", "cfg4"):
+    _c = copy.deepcopy(CONFIGS[_n])
+    _c["eq"]["shared"] = 1
+    CONFIGS[_n + "_sh"] = _c
+
 # cfg5: throughput sweep on the cfg2 equation (BASELINE.json configs[4]).
 CFG5_NODES = (64, 1024, 16384)
 CFG5_TREES = (10_000, 1_000_000, 10_000_000)
