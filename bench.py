@@ -281,6 +281,13 @@ def main():
     peak = N_SM * FP64_LANES * F_MAX_MHZ * 1e6 / 1e12       # T lane-ops/s
     achieved = ops / (walk_avg / 1e3) / 1e12
     clocks = clk.summary()
+    # DRAM traffic of the tree-walk launch from the committed ncu capture of
+    # this same command (profiles/r1/traffic_<workload>.json), else null
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "r1", f"traffic_{cfg['name']}.json")
+    if os.path.exists(tf) and not args.trees:
+        tj = json.load(open(tf))
+        traffic = tj["dram_bytes_read"] + tj["dram_bytes_write"]
 
     # ---- end to end through the public host API (rt_interface_values) -----
     e2e = None
@@ -335,7 +342,8 @@ def main():
         "pruned_fraction": st_one["pruned"] / max(1, st_one["trees"]),
         "roofline": {"bound": "alu", "kernel": "tree_walk_kernel", "achieved": achieved,
                      "peak": peak, "unit": "T FP64 lane-ops/s", "frac": achieved / peak,
-                     "traffic": None, "launch_ms": walk_avg,
+                     "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read + write)",
+                     "launch_ms": walk_avg,
                      "algorithmic_fp64_ops_per_launch": ops,
                      "peak_basis": "148 SM x 64 FP64 lanes/clk x 1965 MHz (B200_PROFILING.md nominal; MEASURED_PEAKS.json has no FP64 entry)",
                      "frac_at_measured_clock": (achieved / (N_SM * FP64_LANES * clocks["sm_mhz"] * 1e6 / 1e12)
