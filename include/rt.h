@@ -106,7 +106,7 @@ typedef struct {
   int32_t coef_axis;    /* a: the coordinate of the variable factor                */
   double  coef_scale;   /* s > 0                                                   */
   double  coef_t0;      /* t0 > 0                                                  */
-  int32_t shared;       /* 1: shared trees (NEXT row f4, DESIGN.md §13): the random  */
+  int32_t shared;       /* 1: shared trees (NEXT row f4, DESIGN.md §12): the random  */
                         /* numbers omit the node index, every node sees the same   */
                         /* trees, leaves evaluated at x_i + δ; unbiased per node,  */
                         /* correlated across nodes; constant coefficients, FP64    */
@@ -238,7 +238,7 @@ rt_status rt_philox_dev(uint64_t key, const uint32_t* d_ctr, int64_t n, uint32_t
 
 /* ------------------------------------------------------------------------
  * NEXT row f1 — probabilistic domain decomposition downstream (PAPER.md:936-950,
- * 1007-1012; DESIGN.md §12), d = 2 with constant coefficients: the square
+ * 1007-1012; DESIGN.md §11), d = 2 with constant coefficients: the square
  * [lo, hi]² is cut by the artificial interfaces x = mid and y = mid
  * (mid = (lo+hi)/2) into four subdomains.  Six lines carry nodal points s_j =
  * lo + j (hi−lo)/(n_s−1) at time levels t_k = k T/(n_t−1): 0 interface x = mid

@@ -171,7 +171,7 @@ def single_domain(g, b, D: float, L: float, h: float, T: float, n_steps: int):
 
 
 # ---------------------------------------------------------------------------
-# the PDD downstream of rt_pdd_downstream_dev, written plainly (DESIGN.md §12)
+# the PDD downstream of rt_pdd_downstream_dev, written plainly (DESIGN.md §11)
 def g_fn(eq):
     """u(x, y, 0) for the equation dict (the four data shapes)."""
     a, s = eq["init_amp"], eq["init_scale"]

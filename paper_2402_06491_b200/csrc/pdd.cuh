@@ -1,5 +1,5 @@
 // pdd.cuh — probabilistic domain decomposition downstream (NEXT row f1,
-// DESIGN.md §12): the interface values produced by the tree walk are turned
+// DESIGN.md §11): the interface values produced by the tree walk are turned
 // into Dirichlet data and four fully decoupled subdomain solves
 // ("Interpolation" and "Local solver", 1007-1012).
 //

@@ -878,7 +878,7 @@ extern "C" rt_status rt_philox_dev(uint64_t key, const uint32_t* d_ctr, int64_t 
 }
 
 // ---------------------------------------------------------------------------
-// NEXT row f1: PDD downstream (pdd.cuh; DESIGN.md §12)
+// NEXT row f1: PDD downstream (pdd.cuh; DESIGN.md §11)
 static rt_status check_pdd(const rt_handle* h, const rt_pdd_cfg* c) {
   if (!c) return fail(RT_E_ARG, "null cfg");
   if (h) {

@@ -184,7 +184,7 @@ __host__ __device__ constexpr int smem_bytes() {
 // SB = Strategy B: a particle is a leaf with probability
 // q (ξ = 0, weight g/q), else it splits after the uniform fraction S of its
 // horizon with weight τ c_k/((1-q) p_k) and its children inherit τ(1-S).
-// SH = shared trees (NEXT row f4, DESIGN.md §13): a task is (32-node tile,
+// SH = shared trees (NEXT row f4, DESIGN.md §12): a task is (32-node tile,
 // tree range); the random numbers omit the node index, so every node sees the
 // same trees; lanes walk different trees carrying the displacement δ from the
 // root, and at every leaf the whole warp evaluates g(x_i + δ) for the tile's

@@ -1,4 +1,4 @@
-"""GPU tests of NEXT row f1 (PDD downstream, DESIGN.md §12) through the C ABI.
+"""GPU tests of NEXT row f1 (PDD downstream, DESIGN.md §11) through the C ABI.
 
 * parity: rt_pdd_downstream_dev on given nodal tables (the exact heat-kernel
   solution, and smooth synthetic tables) against oracle/pdd_oracle.py's

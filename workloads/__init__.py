@@ -144,7 +144,7 @@ for _s, _tag in ((STRAT_A_SHIFT, "A"), (STRAT_B, "B")):
                                 n_trees=1_000_000, seed=0, L=5, M=5)
 
 # NEXT row f4: the BASELINE configs with shared trees (every node sees the
-# same trees; DESIGN.md §13) — a different sampling contract, same per-node law.
+# same trees; DESIGN.md §12) — a different sampling contract, same per-node law.
 for _n in ("cfg2", "cfg3", "cfg4"):
     _c = copy.deepcopy(CONFIGS[_n])
     _c["eq"]["shared"] = 1
