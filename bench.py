@@ -281,6 +281,11 @@ def main():
     peak = N_SM * FP64_LANES * F_MAX_MHZ * 1e6 / 1e12       # T lane-ops/s
     achieved = ops / (walk_avg / 1e3) / 1e12
     clocks = clk.summary()
+    # measured FP64 FMA throughput (K0) beside the nominal peak
+    try:
+        k0 = P.rt.fp64_peak()["lane_ops_per_s"] / 1e12
+    except Exception:   # noqa: BLE001 — diagnostic only
+        k0 = None
     # DRAM traffic of the tree-walk launch from the committed ncu capture of
     # this same command (profiles/r1/traffic_<workload>.json), else null
     traffic = None
@@ -347,7 +352,9 @@ def main():
                      "algorithmic_fp64_ops_per_launch": ops,
                      "peak_basis": "148 SM x 64 FP64 lanes/clk x 1965 MHz (B200_PROFILING.md nominal; MEASURED_PEAKS.json has no FP64 entry)",
                      "frac_at_measured_clock": (achieved / (N_SM * FP64_LANES * clocks["sm_mhz"] * 1e6 / 1e12)
-                                                if clocks.get("sm_mhz") else None)},
+                                                if clocks.get("sm_mhz") else None),
+                     "peak_measured_dfma": k0,
+                     "frac_of_measured_dfma": achieved / k0 if k0 else None},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "clocks": clocks,

@@ -279,6 +279,12 @@ rt_status rt_pdd_downstream_dev(rt_handle* h, const rt_pdd_cfg* cfg, const doubl
 rt_status rt_pdd_solve(rt_handle* h, const rt_pdd_cfg* cfg, double* out_field, double* out_nodal,
                        double* out_ms);
 
+/* Measured FP64 FMA throughput of the current GPU (FP64 lane-ops/s; one
+ * DFMA = one lane-op): 8 CTAs of 256 threads per SM, 8 independent DFMA
+ * chains per thread, CUDA events around one launch.  The measured companion
+ * of the nominal FP64 roofline.  out_ms may be NULL. */
+rt_status rt_fp64_peak(double* out_lane_ops_per_s, double* out_ms);
+
 /* Thread-local message of the last failure on this thread ("" if none). */
 const char* rt_last_error(void);
 

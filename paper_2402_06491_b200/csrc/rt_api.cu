@@ -1058,3 +1058,50 @@ extern "C" rt_status rt_pdd_solve(rt_handle* h, const rt_pdd_cfg* cfg, double* o
   cudaEventDestroy(e1);
   return RT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// K0: measured FP64 FMA throughput of this GPU — the measured
+// companion of the nominal FP64 roofline (148 SMs x 64 lanes x clock).  Every
+// thread runs 8 independent DFMA chains (enough ILP to saturate the pipe at
+// full occupancy); one DFMA = one FP64 lane-op, the unit of bench.py's roofline.
+__global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x * 1e-3, x1 = x0 + 1.0, x2 = x0 + 2.0, x3 = x0 + 3.0;
+  double x4 = x0 + 4.0, x5 = x0 + 5.0, x6 = x0 + 6.0, x7 = x0 + 7.0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  const double s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+  if (s == 1.2345) out[0] = s;   // keep the chains alive
+}
+
+extern "C" rt_status rt_fp64_peak(double* out_lane_ops_per_s, double* out_ms) {
+  if (!out_lane_ops_per_s) return fail(RT_E_ARG, "null pointer");
+  int dev = 0, nsm = 0;
+  RT_CUDA(cudaGetDevice(&dev));
+  RT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  double* d = nullptr;
+  RT_CUDA(cudaMalloc(&d, sizeof(double)));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = nsm * 8, threads = 256, iters = 4096;
+  fp64_peak_kernel<<<blocks, threads>>>(d, 64, 0.999999, 1e-7);   // warm-up
+  cudaEventRecord(e0);
+  fp64_peak_kernel<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
+  cudaEventRecord(e1);
+  cudaError_t e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(RT_E_CUDA, "rt_fp64_peak: %s", cudaGetErrorString(e));
+  const double ops = static_cast<double>(blocks) * threads * iters * 16.0 * 8.0;
+  *out_lane_ops_per_s = ops / (ms * 1e-3);
+  if (out_ms) *out_ms = ms;
+  return RT_OK;
+}

@@ -25,7 +25,7 @@ PREC_FP64, PREC_FP32_POS = 0, 1
 SYMBOLS = ("rt_create", "rt_destroy", "rt_estimate", "rt_estimate_dev", "rt_sums_dev",
            "rt_finalize_dev", "rt_pade", "rt_pade_dev", "rt_interface_values", "rt_trace_dev",
            "rt_get_stats", "rt_set_launch", "rt_set_pool", "rt_philox_dev", "rt_last_error",
-           "rt_pdd_nodes", "rt_pdd_downstream_dev", "rt_pdd_solve")
+           "rt_pdd_nodes", "rt_pdd_downstream_dev", "rt_pdd_solve", "rt_fp64_peak")
 
 
 class RTError(RuntimeError):
@@ -102,6 +102,7 @@ def lib():
             "rt_pdd_nodes": ([C.POINTER(PddCfg), dp]),
             "rt_pdd_downstream_dev": ([H, C.POINTER(PddCfg), dp, dp, dp, vp]),
             "rt_pdd_solve": ([H, C.POINTER(PddCfg), dp, dp, dp]),
+            "rt_fp64_peak": ([C.POINTER(C.c_double), C.POINTER(C.c_double)]),
             "rt_philox_dev": ([u64, vp, i64, vp, vp]),
         }
         for name, args in sig.items():
@@ -352,3 +353,10 @@ def pdd_nodes(cfg: dict) -> np.ndarray:
     out = np.empty((6, cfg["n_s"], 2))
     _check(lib().rt_pdd_nodes(C.byref(pdd_cfg(cfg)), _ptr(out)))
     return out
+
+
+def fp64_peak() -> dict:
+    """rt_fp64_peak: measured FP64 FMA throughput (lane-ops/s) of cuda:current."""
+    v, ms = C.c_double(), C.c_double()
+    _check(lib().rt_fp64_peak(C.byref(v), C.byref(ms)))
+    return dict(lane_ops_per_s=v.value, ms=ms.value)
