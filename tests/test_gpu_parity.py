@@ -499,3 +499,21 @@ def test_example5_gpu_vs_fd_1d_slice(P):
         _, _, us, ses = P.finalize(s, eq["K"], 200_000)
         z = (us.cpu().numpy() - ref) / ses.cpu().numpy()
         assert np.all(np.abs(z) < 4.0), (strat, z)
+
+
+@pytest.mark.parametrize("eq_kw,t,N", [
+    # β = 3 (k up to 8), K = 18: labels of 1 + 54 = 55 bits (limit 56)
+    (dict(dim=1, degree=8, b=[0.0, -1.0, 0.1, 0.1, 0.1, 0.1, 0.1, 0.1, 0.2], K=18), 1.5, 400),
+    # binary KPP at t = 3, K = 30: deep stacks (β = 1, 31-bit labels), heavy pruning
+    (dict(dim=2, degree=2, b=[0.0, -1.0, 1.0] + [0.0] * 6, K=30), 3.0, 300),
+])
+def test_extreme_labels_and_depth(P, orc, eq_kw, t, N):
+    eq = dict(W.get("cfg2")["eq"])
+    eq.update(eq_kw)
+    eq["b"] = list(eq["b"]) + [0.0] * (9 - len(eq["b"]))
+    pts = W.random_nodes(5, eq["dim"], 21)
+    for pool in (0, 4):
+        est = P.Estimator(eq)
+        est.set_pool(pool)
+        rec, _ = est.trace(dev(pts), t, N, seed=31)
+        assert_trees_equal(rec, orc.trees(eq, pts, t, N, seed=31), eq["K"])
