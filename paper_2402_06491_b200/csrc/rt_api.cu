@@ -1009,9 +1009,14 @@ extern "C" rt_status rt_pdd_solve(rt_handle* h, const rt_pdd_cfg* cfg, double* o
   double* sums = static_cast<double*>(h->sums.p);
   RT_CUDA(cudaMemcpyAsync(d_pts, pts.data(), pts.size() * sizeof(double), cudaMemcpyHostToDevice, st));
   RT_CUDA(cudaMemsetAsync(V, 0, static_cast<size_t>(6) * nt * ns * sizeof(double), st));
-  cudaEvent_t e0, e1;
-  RT_CUDA(cudaEventCreate(&e0));
-  RT_CUDA(cudaEventCreate(&e1));
+  // phase events, released on every exit path
+  struct Events {
+    cudaEvent_t e[2] = {nullptr, nullptr};
+    ~Events() { for (cudaEvent_t x : e) if (x) cudaEventDestroy(x); }
+  } ev;
+  RT_CUDA(cudaEventCreate(&ev.e[0]));
+  RT_CUDA(cudaEventCreate(&ev.e[1]));
+  cudaEvent_t e0 = ev.e[0], e1 = ev.e[1];
   RT_CUDA(cudaEventRecord(e0, st));
   pdd_init_kernel<<<(6 * ns + 127) / 128, 128, 0, st>>>(d_pts, V, ns, nt, pdd_eq(h->p));
   RT_CUDA(cudaGetLastError());
@@ -1054,8 +1059,6 @@ extern "C" rt_status rt_pdd_solve(rt_handle* h, const rt_pdd_cfg* cfg, double* o
     RT_CUDA(cudaEventElapsedTime(&c, h->ev[3], h->ev[2]));
     out_ms[0] = a; out_ms[1] = b; out_ms[2] = c;
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   return RT_OK;
 }
 
