@@ -214,3 +214,25 @@ def test_shared_trees_heat_kernel_2d(orc):
 def test_shared_rejects_variable_coefficients(orc):
     with pytest.raises(ValueError):
         orc.normalize(_eq((0.0, 0.0, -1.0), W.STRAT_A_SHIFT, shared=1, coef_kind=[0, 0, 1]))
+
+
+def test_strategy_b_ternary_law_and_mean_leaves(orc):
+    """m = 3 single term (Fig. pkcompare's m = 3 case): a tree
+    with Ne splits has 2Ne + 1 leaves and there are FussCatalan(Ne) =
+    C(3Ne, Ne)/(2Ne + 1) of them, so P(Ne = n) = q^{2n+1} (1-q)^n C(3n,n)/(2n+1);
+    mean leaves (Eq. aproxTb2 context) = q/(1 - m(1-q)) for
+    the unpruned law (q = 0.8 > (m-1)/m keeps it finite)."""
+    from math import comb
+    q = 0.8
+    eq = _eq((0.0, 0.0, 0.0, 1.0), W.STRAT_B, q=q, K=40)
+    qh = orc.normalize(eq)["q_hat"]
+    rec = orc.trees(eq, np.array([[0.0]]), 1.0, 200_000, seed=23)[0]
+    assert np.all(rec["leaves"][rec["pruned"] == 0] == 2 * rec["ne"][rec["pruned"] == 0] + 1)
+    nmax = 8
+    p = np.array([qh ** (2 * n + 1) * (1 - qh) ** n * comb(3 * n, n) / (2 * n + 1) for n in range(nmax)])
+    obs = np.array([np.sum((rec["ne"] == n) & (rec["pruned"] == 0)) for n in range(nmax)])
+    z = (obs - rec.size * p) / np.sqrt(rec.size * p * (1 - p))
+    assert np.all(np.abs(z) < Z), z
+    mean_leaves = qh / (1.0 - 3.0 * (1.0 - qh))
+    se = rec["leaves"].std() / np.sqrt(rec.size)
+    assert abs(rec["leaves"].mean() - mean_leaves) < Z * se + 1e-3, (rec["leaves"].mean(), mean_leaves)
