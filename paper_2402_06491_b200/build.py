@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "librt.so")
 SOURCES = [os.path.join(CSRC, "rt_api.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("tree_walk.cuh", "philox.cuh", "rt_math.cuh", "rt_math_tables.h", "pdd.cuh")] + \
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("tree_walk.cuh", "philox.cuh", "rt_math.cuh", "rt_math_tables.h", "pdd.cuh", "shared_eval.cuh")] + \
     [os.path.join(ROOT, "include", "rt.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -19,6 +19,7 @@
 #include "philox.cuh"
 #include "tree_walk.cuh"
 #include "pdd.cuh"
+#include "shared_eval.cuh"
 
 using rtk::WalkParams;
 
@@ -87,7 +88,7 @@ struct rt_handle {
   cudaStream_t last_stream = nullptr;
   bool have_timing = false;
   double host_total_ms = -1.0;
-  DevBuf partials, gpool, gaux, wtime, pdd_pts, pdd_nodal, pdd_bc, pdd_field, pdd_c, pdd_u, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
+  DevBuf partials, gpool, gaux, wtime, sh_tsum, sh_leaves, pdd_pts, pdd_nodal, pdd_bc, pdd_field, pdd_c, pdd_u, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
   int32_t grid_override = 0;
   int64_t tpt_override = 0;
   int32_t pool_override = 0;
@@ -223,7 +224,7 @@ extern "C" rt_status rt_destroy(rt_handle* h) {
   if (!h) return RT_OK;
   if (h->own_stream) cudaStreamSynchronize(h->own_stream);
   if (h->last_stream) cudaStreamSynchronize(h->last_stream);
-  for (DevBuf* b : {&h->partials, &h->gpool, &h->gaux, &h->wtime, &h->pdd_pts, &h->pdd_nodal,
+  for (DevBuf* b : {&h->partials, &h->gpool, &h->gaux, &h->wtime, &h->sh_tsum, &h->sh_leaves, &h->pdd_pts, &h->pdd_nodal,
                     &h->pdd_bc, &h->pdd_field, &h->pdd_c, &h->pdd_u, &h->sums, &h->stats, &h->h_points, &h->h_coeffs,
                     &h->h_stderr, &h->h_aux, &h->h_flags})
     b->release();
@@ -264,7 +265,7 @@ static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, bool sb, bool sh
                            KernelFn* prod, int* smem, int* pool_cap) {
 #define RT_K(D, G)                                                              \
   if (dim == D && gk == G) {                                                    \
-    *smem = rtk::smem_bytes_sh<D>(sh, nb);                                      \
+    *smem = rtk::smem_bytes<D>();                                               \
     *pool_cap = rtk::PoolCap<D>::v;                                             \
     if (sh && sb) {                                                             \
       *prod = pick_kernel<D, G, false, false, true, true>();                    \
@@ -409,40 +410,9 @@ static rt_status check_run_args(const rt_handle* h, int64_t n_points, double t,
 }
 
 // Runs the tree walk + task reduction; d_sums receives [n][K+2][3].
-static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points, double t,
-                          int64_t tree_offset, int64_t n_trees, uint64_t seed, int rec_shift,
-                          rtk::TreeRec* d_recs, double* d_sums, cudaStream_t st) {
+static void fill_params(const rt_handle* h, WalkParams& P, double t, uint64_t seed) {
   const rt_eq_params& p = h->p;
   const Norm& nz = h->nz;
-  int smem = 0, pool_cap = 0;
-  KernelFn prod = nullptr;
-  const bool sh = p.shared != 0;
-  KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, p.precision == RT_PREC_FP32_POS,
-                           p.strategy == RT_STRATEGY_B, sh, p.K + 2, &prod, &smem, &pool_cap);
-  if (!fn) return fail(RT_E_ARG, "no kernel for dim=%d init_kind=%d", p.dim, p.init_kind);
-  if (smem > 48 * 1024) {
-    RT_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    RT_CUDA(cudaFuncSetAttribute((const void*)prod, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  }
-  Launch L;
-  // shared trees: a task is (32-node tile, tree range)
-  const int64_t n_units = sh ? (n_points + 31) / 32 : n_points;
-  rt_status s = plan_launch(h, prod, smem, n_units, n_trees, L);   // same grid for the trace
-  if (s != RT_OK) return s;
-  const int nb = p.K + 2;
-  const int nf = p.dim + 2;
-  // partials are per node in either mode: [n_points][tpn][nb][3]
-  RT_CUDA(h->partials.ensure(static_cast<size_t>(n_points) * L.tpn * nb * 3 * sizeof(double)));
-  // overflow stack entries once a warp's shared-memory pool is exhausted: a
-  // lane's stack never exceeds K groups, so 32 (K+1) entries per warp always
-  // suffice: [warps][gcap][nf] doubles and [warps][2][gcap] int32
-  const int gcap = 32 * (p.K + 1);
-  const size_t nwarps = static_cast<size_t>(L.grid) * rtk::kWarpsPerCta;
-  RT_CUDA(h->gpool.ensure(nwarps * gcap * nf * sizeof(double)));
-  RT_CUDA(h->gaux.ensure(nwarps * 2 * gcap * sizeof(int32_t)));
-  if (h->pool_override > 0) pool_cap = std::min(pool_cap, static_cast<int>(h->pool_override));
-
-  WalkParams P;
   std::memset(&P, 0, sizeof(P));
   P.rk = rtk::make_round_keys(seed);
   P.inv_lambda = nz.inv_lambda;
@@ -470,10 +440,153 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   P.coef_t0 = p.coef_t0;
   P.tq = nz.tq;
   P.inv_q = p.strategy == RT_STRATEGY_B ? 1.0 / nz.q_hat : 1.0;
-  P.n_points = static_cast<int32_t>(n_points);
   P.beta = nz.beta;
   P.K = p.K;
-  P.nb = nb;
+  P.nb = p.K + 2;
+}
+
+// Shared trees (NEXT row f4): phase 1 walks every tree once
+// (tree_walk_kernel<…, SH>) writing tree summaries and leaf displacements in
+// chunks that fit a memory budget; phase 2 (shared_eval_kernel) evaluates all
+// nodes of every tree; the per-node task reduction is shared.
+template <int DIM, int GK, bool REC>
+static KernelFn eval_kernel() {
+  return reinterpret_cast<KernelFn>(rtk::shared_eval_kernel<DIM, GK, REC>);
+}
+
+static rt_status run_walk_shared(rt_handle* h, KernelFn prod, int smem, int pool_cap,
+                                 const double* d_points, int64_t n_points, double t,
+                                 int64_t tree_offset, int64_t n_trees, uint64_t seed, int rec_shift,
+                                 rtk::TreeRec* d_recs, double* d_sums, cudaStream_t st, int grid) {
+  const rt_eq_params& p = h->p;
+  const Norm& nz = h->nz;
+  const int nb = p.K + 2, nf = p.dim + 2, d = p.dim;
+  int kmax = 0;
+  for (int q = 0; q < nz.n_support; ++q) kmax = std::max(kmax, nz.support[q]);
+  const int lmax = 1 + p.K * std::max(0, kmax - 1);           // leaves of a kept tree
+  const double per_tree = static_cast<double>(lmax) * d * 8 + sizeof(rtk::TreeSum);
+  const int64_t M = std::max<int64_t>(1, std::min<int64_t>(n_trees, static_cast<int64_t>(4.0e9 / per_tree)));
+  const int64_t n_chunks = (n_trees + M - 1) / M;
+  // phase 2 geometry: 64 nodes x tpb trees per CTA, enough CTAs for the GPU
+  const int tiles = static_cast<int>((n_points + 63) / 64);
+  int64_t tpb = M / std::max<int64_t>(1, (148 * 16 + tiles - 1) / tiles);
+  tpb = std::max<int64_t>(128, std::min<int64_t>(tpb, 8192));
+  int64_t tpn_total = 0;
+  for (int64_t c = 0; c < n_chunks; ++c) tpn_total += (std::min(M, n_trees - c * M) + tpb - 1) / tpb;
+  RT_CUDA(h->partials.ensure(static_cast<size_t>(n_points) * tpn_total * nb * 3 * sizeof(double)));
+  RT_CUDA(h->sh_tsum.ensure(static_cast<size_t>(M) * sizeof(rtk::TreeSum)));
+  RT_CUDA(h->sh_leaves.ensure(static_cast<size_t>(M) * lmax * d * sizeof(double)));
+  const int gcap = 32 * (p.K + 1);
+  const size_t nwarps = static_cast<size_t>(grid) * rtk::kWarpsPerCta;
+  RT_CUDA(h->gpool.ensure(nwarps * gcap * nf * sizeof(double)));
+  RT_CUDA(h->gaux.ensure(nwarps * 2 * gcap * sizeof(int32_t)));
+  if (h->pool_override > 0) pool_cap = std::min(pool_cap, static_cast<int>(h->pool_override));
+  KernelFn ev = nullptr, evr = nullptr;
+#define RT_E(D, G) if (p.dim == D && p.init_kind == G) { ev = eval_kernel<D, G, false>(); evr = eval_kernel<D, G, true>(); }
+  RT_E(1, 0) RT_E(1, 1) RT_E(1, 2) RT_E(1, 3) RT_E(2, 0) RT_E(2, 1) RT_E(2, 2) RT_E(2, 3)
+  RT_E(3, 0) RT_E(3, 1) RT_E(3, 2) RT_E(3, 3)
+#undef RT_E
+  const int esmem = nb * 2 * rtk::kEvalThreads * 8;
+  RT_CUDA(cudaFuncSetAttribute((const void*)ev, cudaFuncAttributeMaxDynamicSharedMemorySize, esmem));
+
+  WalkParams P;
+  fill_params(h, P, t, seed);
+  P.points = d_points;
+  P.n_points = static_cast<int32_t>(n_points);
+  P.pool_cap = pool_cap;
+  P.gpool = static_cast<double*>(h->gpool.p);
+  P.gaux = static_cast<int32_t*>(h->gaux.p);
+  P.gcap = gcap;
+  P.stats = static_cast<unsigned long long*>(h->stats.p);
+  P.task_ctr = reinterpret_cast<unsigned int*>(P.stats + 5);
+  P.tsum = static_cast<rtk::TreeSum*>(h->sh_tsum.p);
+  P.leaves = static_cast<double*>(h->sh_leaves.p);
+  P.lmax = lmax;
+  rtk::EvalParams E;
+  std::memset(&E, 0, sizeof(E));
+  E.tsum = P.tsum; E.leaves = P.leaves; E.lmax = lmax; E.tpb = static_cast<int32_t>(tpb);
+  E.points = d_points; E.n_points = static_cast<int32_t>(n_points); E.K = p.K; E.nb = nb;
+  E.amp = P.amp; E.inv_scale = P.inv_scale; E.inv_scale2 = P.inv_scale2;
+  E.partials = static_cast<double*>(h->partials.p); E.tpn_total = tpn_total;
+  E.recs = d_recs; E.rec_shift = rec_shift;
+  E.n_rec = (n_trees + (int64_t(1) << rec_shift) - 1) >> rec_shift;
+
+  RT_CUDA(cudaMemsetAsync(h->stats.p, 0, 6 * sizeof(unsigned long long), st));
+  RT_CUDA(cudaEventRecord(h->ev[0], st));
+  int64_t q0 = 0;
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    const int64_t Mc = std::min(M, n_trees - c * M);
+    // phase 1: tasks are tree ranges of one "unit"; ~8 tasks per warp
+    const int64_t T1 = std::max<int64_t>(32, std::min<int64_t>(4096, Mc / static_cast<int64_t>(nwarps * 8)));
+    P.n_trees = static_cast<int32_t>(Mc);
+    P.tree_offset = static_cast<uint32_t>(tree_offset + c * M);
+    P.T = static_cast<int32_t>(T1);
+    P.tpn = static_cast<int32_t>((Mc + T1 - 1) / T1);
+    P.n_tasks = P.tpn;
+    RT_CUDA(cudaMemsetAsync(P.task_ctr, 0, sizeof(unsigned int), st));
+    const int g1 = static_cast<int>(std::min<int64_t>(grid, (P.n_tasks + rtk::kWarpsPerCta - 1) / rtk::kWarpsPerCta));
+    prod<<<g1, rtk::kThreads, smem, st>>>(P);
+    RT_CUDA(cudaGetLastError());
+    // phase 2: every node of every tree of the chunk
+    E.M = Mc;
+    E.q0 = q0;
+    E.rel0 = static_cast<uint32_t>(c * M);
+    const dim3 eg(static_cast<unsigned>(tiles), static_cast<unsigned>((Mc + tpb - 1) / tpb));
+    reinterpret_cast<void (*)(rtk::EvalParams)>(ev)<<<eg, rtk::kEvalThreads, esmem, st>>>(E);
+    RT_CUDA(cudaGetLastError());
+    if (d_recs) {
+      reinterpret_cast<void (*)(rtk::EvalParams)>(evr)<<<eg, rtk::kEvalThreads, 0, st>>>(E);
+      RT_CUDA(cudaGetLastError());
+    }
+    q0 += eg.y;
+  }
+  RT_CUDA(cudaEventRecord(h->ev[1], st));
+  reduce_tasks_kernel<<<static_cast<unsigned>(n_points), 32, 0, st>>>(
+      static_cast<double*>(h->partials.p), tpn_total, nb, d_sums,
+      static_cast<unsigned long long*>(h->stats.p));
+  RT_CUDA(cudaGetLastError());
+  h->last_stream = st;
+  h->have_timing = true;
+  h->host_total_ms = -1.0;
+  return RT_OK;
+}
+
+static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points, double t,
+                          int64_t tree_offset, int64_t n_trees, uint64_t seed, int rec_shift,
+                          rtk::TreeRec* d_recs, double* d_sums, cudaStream_t st) {
+  const rt_eq_params& p = h->p;
+  const Norm& nz = h->nz;
+  int smem = 0, pool_cap = 0;
+  KernelFn prod = nullptr;
+  const bool sh = p.shared != 0;
+  KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, p.precision == RT_PREC_FP32_POS,
+                           p.strategy == RT_STRATEGY_B, sh, p.K + 2, &prod, &smem, &pool_cap);
+  if (!fn) return fail(RT_E_ARG, "no kernel for dim=%d init_kind=%d", p.dim, p.init_kind);
+  if (smem > 48 * 1024) {
+    RT_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    RT_CUDA(cudaFuncSetAttribute((const void*)prod, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  }
+  Launch L;
+  rt_status s = plan_launch(h, prod, smem, n_points, n_trees, L);   // same grid for the trace
+  if (s != RT_OK) return s;
+  if (sh) return run_walk_shared(h, prod, smem, pool_cap, d_points, n_points, t, tree_offset, n_trees,
+                                 seed, rec_shift, d_recs, d_sums, st, L.grid);
+  const int nb = p.K + 2;
+  const int nf = p.dim + 2;
+  // partials are per node in either mode: [n_points][tpn][nb][3]
+  RT_CUDA(h->partials.ensure(static_cast<size_t>(n_points) * L.tpn * nb * 3 * sizeof(double)));
+  // overflow stack entries once a warp's shared-memory pool is exhausted: a
+  // lane's stack never exceeds K groups, so 32 (K+1) entries per warp always
+  // suffice: [warps][gcap][nf] doubles and [warps][2][gcap] int32
+  const int gcap = 32 * (p.K + 1);
+  const size_t nwarps = static_cast<size_t>(L.grid) * rtk::kWarpsPerCta;
+  RT_CUDA(h->gpool.ensure(nwarps * gcap * nf * sizeof(double)));
+  RT_CUDA(h->gaux.ensure(nwarps * 2 * gcap * sizeof(int32_t)));
+  if (h->pool_override > 0) pool_cap = std::min(pool_cap, static_cast<int>(h->pool_override));
+
+  WalkParams P;
+  fill_params(h, P, t, seed);
+  P.n_points = static_cast<int32_t>(n_points);
   P.points = d_points;
   P.n_trees = static_cast<int32_t>(n_trees);
   P.tree_offset = static_cast<uint32_t>(tree_offset);

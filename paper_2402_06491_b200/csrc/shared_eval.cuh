@@ -1,0 +1,108 @@
+// shared_eval.cuh — shared trees (NEXT row f4), phase 2.
+//
+// Phase 1 (tree_walk_kernel<…, SH = true>) walked every tree ONCE for all
+// nodes and stored its summary (order bin, weight product W, leaf count) and
+// its leaf displacements δ_l from the root.  Here a CTA of 64 threads takes
+// 64 nodes (thread = node) and a block of consecutive trees; every thread
+// runs the same trees in index order, so control flow is identical across
+// the warp and the tree data are warp-uniform loads (L1/L2 broadcasts):
+//   C_i = W · Π_l g(x_i + δ_l)  (leaves at x_i + δ),
+// accumulated into the node's order bin (ΣC, ΣC²; counts are node-free).
+// The loop is the g evaluations themselves — FP64-pipe bound.  Results per
+// (node, tree block) go to the per-node task partials that the shared task
+// reduction sums in block order (deterministic).
+#pragma once
+#include <cstdint>
+
+#include "tree_walk.cuh"
+
+namespace rtk {
+
+constexpr int kEvalThreads = 64;
+
+struct EvalParams {
+  const TreeSum* tsum;
+  const double* leaves;      // [M][lmax][DIM]
+  int32_t lmax;
+  int64_t M;                 // trees in this chunk
+  int32_t tpb;               // trees per block (blockIdx.y)
+  const double* points;      // [n_points][DIM]
+  int32_t n_points;
+  int32_t K, nb;
+  double amp, inv_scale, inv_scale2;
+  double* partials;          // [n_points][tpn_total][nb][3]
+  int64_t tpn_total, q0;     // per-node task count, first block index of this chunk
+  TreeRec* recs;             // REC: [n_points][n_rec]
+  int64_t n_rec;
+  int32_t rec_shift;
+  uint32_t rel0;             // REC: tree index of this chunk relative to the call's first tree
+};
+
+template <int DIM, int GK, bool REC>
+__global__ void __launch_bounds__(kEvalThreads)
+shared_eval_kernel(const __grid_constant__ EvalParams E) {
+  extern __shared__ double acc[];                 // [nb][2][kEvalThreads]
+  __shared__ int cnt[32];
+  const int tid = threadIdx.x;
+  const int node = blockIdx.x * kEvalThreads + tid;
+  const bool valid = node < E.n_points;
+  double x[DIM];
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) x[k] = valid ? E.points[static_cast<int64_t>(node) * DIM + k] : 0.0;
+  if constexpr (!REC) {
+    for (int q = tid; q < E.nb * 2 * kEvalThreads; q += kEvalThreads) acc[q] = 0.0;
+    if (tid < 32) cnt[tid] = 0;
+    __syncthreads();
+  }
+  WalkParams G;                                   // g_eval's parameters
+  G.amp = E.amp; G.inv_scale = E.inv_scale; G.inv_scale2 = E.inv_scale2;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.y) * E.tpb;
+  const int64_t j1 = min(E.M, j0 + E.tpb);
+  for (int64_t j = j0; j < j1; ++j) {
+    const TreeSum ts = E.tsum[j];                 // warp-uniform
+    if constexpr (REC) {
+      const uint32_t rel = E.rel0 + static_cast<uint32_t>(j);
+      if ((rel & ((1u << E.rec_shift) - 1u)) != 0u) continue;
+    }
+    double C = 0.0;
+    if (ts.bin <= E.K) {
+      double prod = ts.W;
+      const double* lf = E.leaves + j * E.lmax * DIM;
+      for (int l = 0; l < ts.nl; ++l) {
+        double xe[DIM];
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) xe[k] = x[k] + lf[l * DIM + k];
+        prod *= g_eval<DIM, GK>(xe, G);
+      }
+      C = prod;
+      if constexpr (!REC) {
+        acc[(ts.bin * 2 + 0) * kEvalThreads + tid] += C;
+        acc[(ts.bin * 2 + 1) * kEvalThreads + tid] = fma(C, C, acc[(ts.bin * 2 + 1) * kEvalThreads + tid]);
+      }
+    }
+    if constexpr (REC) {
+      if (valid) {
+        TreeRec r;
+        r.ne = ts.ne; r.leaves = ts.nl; r.particles = ts.parts; r.pruned = ts.bin > E.K ? 1 : 0;
+        r.C = C;
+        const uint32_t rel = E.rel0 + static_cast<uint32_t>(j);
+        E.recs[static_cast<int64_t>(node) * E.n_rec + (rel >> E.rec_shift)] = r;
+      }
+    } else {
+      if (tid == 0) cnt[ts.bin] += 1;
+    }
+  }
+  if constexpr (!REC) {
+    __syncthreads();
+    if (valid) {
+      double* o = E.partials + (static_cast<int64_t>(node) * E.tpn_total + E.q0 + blockIdx.y) * E.nb * 3;
+      for (int b = 0; b < E.nb; ++b) {
+        o[b * 3 + 0] = acc[(b * 2 + 0) * kEvalThreads + tid];
+        o[b * 3 + 1] = acc[(b * 2 + 1) * kEvalThreads + tid];
+        o[b * 3 + 2] = static_cast<double>(cnt[b]);
+      }
+    }
+  }
+}
+
+}  // namespace rtk

@@ -64,6 +64,14 @@ struct TreeRec {   // mirrors rt_tree_rec
   double C;
 };
 
+// Shared trees (f4): what phase 2 needs of a tree — its order bin (K+1 if
+// pruned), leaf count, splits, particles and the node-free weight product W
+// (root factor × split weights × Strategy B's 1/q per leaf).
+struct TreeSum {
+  int32_t bin, nl, ne, parts;
+  double W;
+};
+
 struct WalkParams {
   RoundKeys rk;
   double inv_lambda, two_d, amp, inv_scale, inv_scale2, t;
@@ -94,7 +102,12 @@ struct WalkParams {
   double coef_inv_s2, coef_t0;
   uint32_t tq;                 // Strategy B: leaf iff block-0 word 3 < tq
   double inv_q;                // Strategy B: 1/q̂
-  int32_t n_points;            // shared trees (f4): nodes; tasks = 32-node tiles x tree ranges
+  int32_t n_points;            // nodes (shared trees: the stats are per (node, tree))
+  // shared trees (f4), phase 1: per-tree summaries and leaf displacements of
+  // trees [tree_offset, tree_offset + n_trees): tsum[j], leaves[j][lmax][DIM]
+  struct TreeSum* tsum;
+  double* leaves;
+  int32_t lmax;
   unsigned long long* wtime;   // debug (RT_WARP_TIMES): [warps][4] start, end, smid, iterations; or null
 };
 
@@ -184,13 +197,13 @@ __host__ __device__ constexpr int smem_bytes() {
 // SB = Strategy B: a particle is a leaf with probability
 // q (ξ = 0, weight g/q), else it splits after the uniform fraction S of its
 // horizon with weight τ c_k/((1-q) p_k) and its children inherit τ(1-S).
-// SH = shared trees (NEXT row f4): a task is (32-node tile,
-// tree range); the random numbers omit the node index, so every node sees the
-// same trees; lanes walk different trees carrying the displacement δ from the
-// root, and at every leaf the whole warp evaluates g(x_i + δ) for the tile's
-// 32 nodes (lane = node).  Constant coefficients only (weights node-free).
+// SH = shared trees (NEXT row f4), phase 1: the random numbers
+// omit the node index, so every node sees the same trees; a task is a tree
+// range; lanes walk trees carrying the displacement δ from the root and write
+// each tree's summary (TreeSum) and leaf displacements; phase 2
+// (shared_eval.cuh) evaluates all nodes.  Constant coefficients only.
 template <int DIM, int GK, bool REC, bool F32, bool SB, bool SH>
-__global__ void __launch_bounds__(kThreads, SH ? 2 : MinCtas<DIM, REC>::v)
+__global__ void __launch_bounds__(kThreads, MinCtas<DIM, REC>::v)
 tree_walk_kernel(const __grid_constant__ WalkParams P) {
   using PT = typename std::conditional<F32, float, double>::type;   // position type
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -202,7 +215,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 
   // ---- shared memory carve-up -------------------------------------------
   LogEntry* const ltab = reinterpret_cast<LogEntry*>(smem_raw);
-  const int wstride = SH ? warp_stride<DIM>(true, P.nb) : warp_stride<DIM>(false, 0);
+  const int wstride = warp_stride<DIM>(false, 0);
   unsigned char* const wbase = smem_raw + 128 * 16 + wib * wstride;
   double* const pool = reinterpret_cast<double*>(wbase);                   // [NF][CAP]
   double* const ringC = pool + NF * CAP;                                    // [kRing]
@@ -214,11 +227,6 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   uint8_t* const freeS = reinterpret_cast<uint8_t*>(prevS + CAP);           // [CAP]
   double* const wtab = reinterpret_cast<double*>(smem_raw + 128 * 16 +
       kWarpsPerCta * wstride);                                           // [9] weights
-  // shared-tree mode extras (SH), after the warp's common region
-  double* const shPi = reinterpret_cast<double*>(wbase + (warp_smem_bytes<DIM>() + 15) / 16 * 16);  // [32 trees][32 nodes]
-  double* const shAcc = shPi + 32 * 32;                                     // [nb][2][32 nodes]
-  int* const shCnt = reinterpret_cast<int*>(shAcc + (SH ? P.nb : 0) * 2 * 32);  // [32 bins]
-  double* const shNode = reinterpret_cast<double*>(shCnt + 32);             // [DIM][32]
   int* const ktab = reinterpret_cast<int*>(wtab + 9);                     // [9] offspring k
   for (int q = threadIdx.x; q < 128; q += kThreads) ltab[q] = kLogTable[q];
   if (threadIdx.x < 9) {
@@ -230,11 +238,6 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   bsum[lane] = 0.0;
   bsum[32 + lane] = 0.0;
   bcnt[lane] = 0;
-  if constexpr (SH) {
-    for (int f = 0; f < 32; ++f) shPi[f * 32 + lane] = 1.0;
-    for (int q = 0; q < 2 * P.nb; ++q) shAcc[q * 32 + lane] = 0.0;
-    shCnt[lane] = 0;
-  }
 
   const int gwarp = blockIdx.x * kWarpsPerCta + wib;
   if (P.wtime != nullptr && lane == 0) P.wtime[4 * gwarp] = global_ns();
@@ -252,7 +255,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   // absorbs the warp scheduler's unequal issue rates.
   uint32_t iss_next = 0u, iss_end = 0u, iss_node = 0u;
   int task = -1, left = 0;             // current task, its trees not yet recorded
-  int task_q = 0, tile_n = 0;          // SH: tree-range index, nodes in the tile
+  int task_q = 0;                      // the task's tree-range index
   bool stream_end = false;
   auto next_task = [&]() {             // all lanes, converged
     int t = 0;
@@ -260,20 +263,17 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= P.n_tasks) { stream_end = true; return; }
     task = t;
-    const int node = t / P.tpn;          // SH: the node tile
+    const int node = t / P.tpn;          // SH: always 0 (tasks are tree ranges)
     const int q = t - node * P.tpn;
     const int size = min(P.T, P.n_trees - q * P.T);
     task_q = q;
-    iss_node = static_cast<uint32_t>(SH ? node * 32 : node);
+    iss_node = static_cast<uint32_t>(node);
     iss_next = static_cast<uint32_t>(P.tree_offset) + static_cast<uint32_t>(q * P.T);
     iss_end = iss_next + static_cast<uint32_t>(size);
     left = size;
     __syncwarp();
     if constexpr (SH) {
-      tile_n = min(32, P.n_points - node * 32);
-#pragma unroll
-      for (int k = 0; k < DIM; ++k)
-        shNode[k * 32 + lane] = lane < tile_n ? P.points[static_cast<int64_t>(node * 32 + lane) * DIM + k] : 0.0;
+      // the walk carries δ from the root: no node coordinates
     } else if (lane == 0) {
 #pragma unroll
       for (int k = 0; k < DIM; ++k) ws->iss_y[k] = P.points[static_cast<int64_t>(node) * DIM + k];
@@ -302,7 +302,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 #pragma unroll
     for (int k = 0; k < DIM; ++k) y[k] = SH ? PT(0) : static_cast<PT>(ws->iss_y[k]);   // SH: δ = 0
     tau = P.t; label = 1; Pi = P.root; ne = 0; top = -1;
-    if constexpr (REC) { leaves = 0; parts = 0; }
+    if constexpr (REC || SH) { leaves = 0; parts = 0; }
     active = true;
   };
 
@@ -336,24 +336,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   // fold the event counters, fetch the next task and start its first trees.
   auto close_and_next = [&]() {
     if constexpr (SH) {
-      // node i of the tile (lane i): partials[(node · tpn + q)][b], the layout
-      // of the per-node tasks, so the task reduction is shared
-      __syncwarp();
-      if (lane < tile_n) {
-        double* o = P.partials + ((static_cast<int64_t>(iss_node) + lane) * P.tpn + task_q) * P.nb * 3;
-        for (int b = 0; b < P.nb; ++b) {
-          o[b * 3 + 0] = shAcc[(b * 2 + 0) * 32 + lane];
-          o[b * 3 + 1] = shAcc[(b * 2 + 1) * 32 + lane];
-          o[b * 3 + 2] = static_cast<double>(shCnt[b]);
-        }
-      }
-      __syncwarp();
-      for (int q = 0; q < 2 * P.nb; ++q) shAcc[q * 32 + lane] = 0.0;
-      shCnt[lane] = 0;
-      // stats per (node, tree) as in the independent mode: every node of the
-      // tile sees each walked particle and leaf (g evaluations = leaves)
-      c_leaf *= static_cast<uint32_t>(tile_n);
-      c_part *= static_cast<uint32_t>(tile_n);
+      // phase 1 writes tree summaries only (phase 2 accumulates per node)
     } else {
       flush();
       if (lane < P.nb) {
@@ -366,7 +349,9 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       bsum[32 + lane] = 0.0;
       bcnt[lane] = 0;
     }
-    unsigned long long v0 = c_part, v1 = c_leaf;
+    // (shared trees: every node sees each walked particle and leaf)
+    const unsigned long long scale = SH ? static_cast<unsigned long long>(P.n_points) : 1ull;
+    unsigned long long v0 = c_part * scale, v1 = c_leaf * scale;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       v0 += __shfl_xor_sync(0xffffffffu, v0, o);
@@ -548,9 +533,9 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     if (active) Pi *= fac;
     c_part += active ? 1u : 0u;
     c_leaf += (active && leaf) ? 1u : 0u;
-    if constexpr (REC) {
+    if constexpr (REC || SH) {
       parts += active ? 1 : 0;
-      leaves += (active && leaf) ? 1 : 0;
+      if constexpr (!SH) leaves += (active && leaf) ? 1 : 0;   // SH counts at the store below
     }
     const bool push = branch && k > 1;           // k-1 younger siblings wait
     const bool pop = (active && leaf) || (branch && k == 0);
@@ -563,32 +548,16 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const uint64_t push_pk = (base | 1ull) | (static_cast<uint64_t>(k - 1) << 56);
     label = base;
 
-    // ---------------- shared trees: g at every leaf for the tile's nodes -------
-    // (before the pops overwrite y): for each leaf lane f, lane i multiplies
-    // g(x_i + δ_f) into its product for tree f; two leaves per step for ILP
+    // ---------------- shared trees, phase 1: store the leaf displacement -------
+    // (before the pops overwrite y): leaves[j][l] = δ of the tree's l-th leaf
     if constexpr (SH) {
-      unsigned lf = __ballot_sync(0xffffffffu, active && leaf);
-      while (lf != 0u) {
-        const int f1 = __ffs(lf) - 1;
-        lf &= lf - 1u;
-        const int f2 = lf != 0u ? __ffs(lf) - 1 : f1;
-        const bool two = lf != 0u;
-        if (two) lf &= lf - 1u;
-        double x1[DIM], x2[DIM];
+      if (active && leaf) {
+        double* const o = P.leaves + (static_cast<int64_t>(tj - static_cast<uint32_t>(P.tree_offset)) *
+                                          P.lmax + leaves) * DIM;
 #pragma unroll
-        for (int k = 0; k < DIM; ++k) {
-          const double yk = static_cast<double>(y[k]);
-          x1[k] = shNode[k * 32 + lane] + __shfl_sync(0xffffffffu, yk, f1);
-          x2[k] = shNode[k * 32 + lane] + __shfl_sync(0xffffffffu, yk, f2);
-        }
-        if (lane < tile_n) {
-          const double g1 = g_eval<DIM, GK>(x1, P);
-          const double g2 = g_eval<DIM, GK>(x2, P);
-          shPi[f1 * 32 + lane] *= g1;
-          if (two) shPi[f2 * 32 + lane] *= g2;
-        }
+        for (int k = 0; k < DIM; ++k) o[k] = static_cast<double>(y[k]);
+        ++leaves;
       }
-      __syncwarp();
     }
 
     // ---------------- stack: push / pop / release -----------------------------
@@ -697,38 +666,13 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       const int nfin = __popc(fin);
       const int rank = __popc(fin & lt_mask);
       if constexpr (SH) {
-        // finished trees in lane order: lane i adds C_i = W_f · Π_f[i] to its
-        // node's bin (deterministic), then resets the product for the lane
-        unsigned ff = fin;
-        const int my_bin = pruned ? (P.K + 1) : ne;
-        while (ff != 0u) {
-          const int f = __ffs(ff) - 1;
-          ff &= ff - 1u;
-          const int bf = __shfl_sync(0xffffffffu, my_bin, f);
-          const double wf = __shfl_sync(0xffffffffu, Pi, f);
-          if (lane < tile_n) {
-            if (bf <= P.K) {
-              const double C = wf * shPi[f * 32 + lane];
-              shAcc[(bf * 2 + 0) * 32 + lane] += C;
-              shAcc[(bf * 2 + 1) * 32 + lane] = fma(C, C, shAcc[(bf * 2 + 1) * 32 + lane]);
-            }
-          }
-          if constexpr (REC) {
-            const uint32_t tf = __shfl_sync(0xffffffffu, tj, f);
-            const int lvf = __shfl_sync(0xffffffffu, leaves, f);
-            const int pvf = __shfl_sync(0xffffffffu, parts, f);
-            const int nef = __shfl_sync(0xffffffffu, ne, f);
-            const uint32_t rel = tf - static_cast<uint32_t>(P.tree_offset);
-            if (lane < tile_n && (rel & ((1u << P.rec_shift) - 1u)) == 0u) {
-              TreeRec r;
-              r.ne = nef; r.leaves = lvf; r.particles = pvf; r.pruned = bf > P.K ? 1 : 0;
-              r.C = bf > P.K ? 0.0 : wf * shPi[f * 32 + lane];
-              P.recs[(static_cast<int64_t>(iss_node) + lane) * P.n_rec + (rel >> P.rec_shift)] = r;
-            }
-          }
-          if (lane == 0) shCnt[bf] += 1;
-          shPi[f * 32 + lane] = 1.0;
-          __syncwarp();
+        // phase 1: the finished tree's summary (phase 2 evaluates the nodes)
+        if (done) {
+          TreeSum ts;
+          ts.bin = pruned ? (P.K + 1) : ne;
+          ts.nl = leaves; ts.ne = ne; ts.parts = parts;
+          ts.W = pruned ? 0.0 : Pi;
+          P.tsum[tj - static_cast<uint32_t>(P.tree_offset)] = ts;
         }
       } else {
         if (done) {
