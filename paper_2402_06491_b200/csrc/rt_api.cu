@@ -450,8 +450,9 @@ static void fill_params(const rt_handle* h, WalkParams& P, double t, uint64_t se
 // chunks that fit a memory budget; phase 2 (shared_eval_kernel) evaluates all
 // nodes of every tree; the per-node task reduction is shared.
 template <int DIM, int GK, bool REC>
-static KernelFn eval_kernel() {
-  return reinterpret_cast<KernelFn>(rtk::shared_eval_kernel<DIM, GK, REC>);
+static KernelFn eval_kernel(int npt) {
+  return npt == 2 ? reinterpret_cast<KernelFn>(rtk::shared_eval_kernel<DIM, GK, REC, 2>)
+                  : reinterpret_cast<KernelFn>(rtk::shared_eval_kernel<DIM, GK, REC, 1>);
 }
 
 static rt_status run_walk_shared(rt_handle* h, KernelFn prod, int smem, int pool_cap,
@@ -467,8 +468,11 @@ static rt_status run_walk_shared(rt_handle* h, KernelFn prod, int smem, int pool
   const double per_tree = static_cast<double>(lmax) * d * 8 + sizeof(rtk::TreeSum);
   const int64_t M = std::max<int64_t>(1, std::min<int64_t>(n_trees, static_cast<int64_t>(4.0e9 / per_tree)));
   const int64_t n_chunks = (n_trees + M - 1) / M;
-  // phase 2 geometry: 64 nodes x tpb trees per CTA, enough CTAs for the GPU
-  const int tiles = static_cast<int>((n_points + 63) / 64);
+  // phase 2 geometry: 64 or 128 nodes (1 or 2 per thread) x tpb trees per
+  // CTA, enough CTAs for the GPU
+  const int npt = n_points >= 256 ? 2 : 1;
+  const int npc = rtk::kEvalThreads * npt;
+  const int tiles = static_cast<int>((n_points + npc - 1) / npc);
   int64_t tpb = M / std::max<int64_t>(1, (148 * 16 + tiles - 1) / tiles);
   tpb = std::max<int64_t>(128, std::min<int64_t>(tpb, 8192));
   int64_t tpn_total = 0;
@@ -482,11 +486,11 @@ static rt_status run_walk_shared(rt_handle* h, KernelFn prod, int smem, int pool
   RT_CUDA(h->gaux.ensure(nwarps * 2 * gcap * sizeof(int32_t)));
   if (h->pool_override > 0) pool_cap = std::min(pool_cap, static_cast<int>(h->pool_override));
   KernelFn ev = nullptr, evr = nullptr;
-#define RT_E(D, G) if (p.dim == D && p.init_kind == G) { ev = eval_kernel<D, G, false>(); evr = eval_kernel<D, G, true>(); }
+#define RT_E(D, G) if (p.dim == D && p.init_kind == G) { ev = eval_kernel<D, G, false>(npt); evr = eval_kernel<D, G, true>(npt); }
   RT_E(1, 0) RT_E(1, 1) RT_E(1, 2) RT_E(1, 3) RT_E(2, 0) RT_E(2, 1) RT_E(2, 2) RT_E(2, 3)
   RT_E(3, 0) RT_E(3, 1) RT_E(3, 2) RT_E(3, 3)
 #undef RT_E
-  const int esmem = nb * 2 * rtk::kEvalThreads * 8;
+  const int esmem = nb * 2 * rtk::kEvalThreads * npt * 8;
   RT_CUDA(cudaFuncSetAttribute((const void*)ev, cudaFuncAttributeMaxDynamicSharedMemorySize, esmem));
 
   WalkParams P;
