@@ -1071,7 +1071,8 @@ static rt_status pdd_downstream(rt_handle* h, const rt_pdd_cfg* cfg, const doubl
   const int smem = rtk::pdd_smem_bytes(G.m);
   RT_CUDA(cudaFuncSetAttribute((const void*)rtk::pdd_adi_kernel,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const int threads = std::min(1024, ((G.m + 1 + 31) / 32) * 32);
+  // the pointwise reaction spreads over many threads; the line sweeps use m-1 of them
+  const int threads = std::min(1024, std::max(256, ((G.m + 1) * (G.m + 1) / 4 + 31) / 32 * 32));
   rtk::pdd_adi_kernel<<<4, threads, smem, st>>>(bc, d_field, G, pdd_eq(h->p));
   RT_CUDA(cudaGetLastError());
   return RT_OK;
