@@ -261,8 +261,8 @@ static KernelFn pick_kernel() {
 
 // The kernel for (dim, g, rec) and the production (rec = false) kernel whose
 // occupancy fixes the launch geometry for both.
-static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, bool sb, bool sh, int nb,
-                           KernelFn* prod, int* smem, int* pool_cap) {
+static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, bool sb, bool sh, KernelFn* prod,
+                           int* smem, int* pool_cap) {
 #define RT_K(D, G)                                                              \
   if (dim == D && gk == G) {                                                    \
     *smem = rtk::smem_bytes<D>();                                               \
@@ -564,7 +564,7 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   KernelFn prod = nullptr;
   const bool sh = p.shared != 0;
   KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, p.precision == RT_PREC_FP32_POS,
-                           p.strategy == RT_STRATEGY_B, sh, p.K + 2, &prod, &smem, &pool_cap);
+                           p.strategy == RT_STRATEGY_B, sh, &prod, &smem, &pool_cap);
   if (!fn) return fail(RT_E_ARG, "no kernel for dim=%d init_kind=%d", p.dim, p.init_kind);
   if (smem > 48 * 1024) {
     RT_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

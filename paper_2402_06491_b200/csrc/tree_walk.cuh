@@ -167,21 +167,9 @@ __host__ __device__ constexpr int warp_smem_bytes() {
          static_cast<int>(sizeof(WarpState));
 }
 
-// Shared-tree mode (NEXT row f4) adds per warp: the per-(tree lane, node)
-// products of g [32][32], the order-bin sums [nb][ΣC, ΣC²][32 nodes], bin
-// counts [32] and the node tile [DIM][32].
-__host__ __device__ constexpr int shared_extra_bytes(int dim, int nb) {
-  return 32 * 32 * 8 + nb * 2 * 32 * 8 + 32 * 4 + dim * 32 * 8;
-}
-
 template <int DIM>
-__host__ __device__ constexpr int warp_stride(bool sh, int nb) {
-  return ((warp_smem_bytes<DIM>() + (sh ? shared_extra_bytes(DIM, nb) : 0)) + 15) / 16 * 16;
-}
-
-template <int DIM>
-__host__ __device__ constexpr int smem_bytes_sh(bool sh, int nb) {
-  return 128 * 16 + kWarpsPerCta * warp_stride<DIM>(sh, nb) + 9 * 8 + 9 * 4;
+__host__ __device__ constexpr int warp_stride() {
+  return (warp_smem_bytes<DIM>() + 15) / 16 * 16;
 }
 
 template <int DIM>
@@ -215,7 +203,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 
   // ---- shared memory carve-up -------------------------------------------
   LogEntry* const ltab = reinterpret_cast<LogEntry*>(smem_raw);
-  const int wstride = warp_stride<DIM>(false, 0);
+  const int wstride = warp_stride<DIM>();
   unsigned char* const wbase = smem_raw + 128 * 16 + wib * wstride;
   double* const pool = reinterpret_cast<double*>(wbase);                   // [NF][CAP]
   double* const ringC = pool + NF * CAP;                                    // [kRing]
