@@ -175,7 +175,8 @@ def run_reference(args, cfg):
             sample = r["sample"]
     tot = sum(times)
     v = trees / tot
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "trees/s", "n_gpus": 0,
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "trees/s", "n_gpus": ws,
+            "host_only": True,   # the oracle runs on one host core, no GPU work
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": _config_json(cfg, ws),
