@@ -273,3 +273,32 @@ def test_prefix_and_offsets(orc):
     # a different seed gives different trees
     c = orc.trees(cfg["eq"], pts, 1.0, 300, seed=6)
     assert not np.array_equal(a["C"], c["C"])
+
+
+@pytest.mark.parametrize("name,u0", [("cfg2", 0.4), ("cfg4", 0.5)])
+def test_second_moments_constant_data(orc, name, u0):
+    """ΣC² per order (the stderr inputs, row a7): for constant data a tree
+    contributes C = Π w_k · u0^{leaves}, so E[C² 1{Ne = n}] is the z^n
+    coefficient of V' = -λV + z Σ_k λ p̂_k w_k² V^k, V(0) = u0² — the same
+    branching law with squared weights (SURVEY §8(c) 'Stderr').  Checked for
+    n <= 6 against the sample mean of C² 1{Ne = n} within 4.5 of its standard
+    errors (a wrong ΣC² accumulation, e.g. C instead of C², fails); at higher
+    orders C² = Π w² u0^{2 leaves} spans dozens of decades within one bin (the
+    leaf count varies) and the sample standard error is no longer a reliable
+    scale, so only ΣC² = Σ C² is asserted there."""
+    cfg = W.get(name)
+    eq = dict(cfg["eq"], init_kind=W.G_CONST, init_amp=u0)
+    K, t, N = eq["K"], cfg["t"], 60_000
+    nz = orc.normalize(eq)
+    a2 = [0.0] * 9
+    for k, ph, w in zip(nz["support"], nz["p_hat"], nz["w"]):
+        a2[k] = nz["lam"] * ph * w * w
+    ex = cf.ode_orders(a2, nz["lam"], u0 * u0, t, K)
+    s, _ = orc.sums(eq, np.zeros((1, eq["dim"])), t, N, seed=17)
+    rec = orc.trees(eq, np.zeros((1, eq["dim"])), t, N, seed=17)[0]
+    for n in range(K + 1):
+        c2 = np.where((rec["ne"] == n) & (rec["pruned"] == 0), rec["C"] ** 2, 0.0)
+        assert np.isclose(c2.sum(), s[0, n, 1], rtol=1e-12, atol=0)      # ΣC² is Σ of C²
+        if n <= 6:
+            se = c2.std() / np.sqrt(N)
+            assert abs(c2.mean() - ex[n]) <= 4.5 * se, (n, c2.mean(), ex[n], se)
