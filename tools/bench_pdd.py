@@ -35,8 +35,8 @@ def main():
     i0 = int(np.argmin(np.abs(x + 2.0)))
     ref = u[i0:i0 + 81, i0:i0 + 81]
     rows = []
-    est = P.Estimator(eq)
-    for boundary in (1, 0):
+    for boundary, shared in ((1, 0), (0, 0), (1, 1)):
+        est = P.Estimator(dict(eq, shared=shared))
         cfg = dict(lo=-2.0, hi=2.0, T=0.5, n_cells=80, n_steps=500, n_s=17, n_t=6, boundary=boundary,
                    L=5, M=5, n_trees=a.trees, seed=7)
         est.pdd_solve(cfg)                          # warm-up
@@ -45,7 +45,8 @@ def main():
         wall = (time.perf_counter() - t0) * 1e3
         d = np.abs(F - ref)
         n_pts = (6 if boundary else 2) * cfg["n_s"] * (cfg["n_t"] - 1)
-        r = dict(workload="cfg3 PDD", boundary=["zero Dirichlet", "probabilistic"][boundary],
+        r = dict(workload="cfg3 PDD" + (" (shared trees)" if shared else ""),
+                 boundary=["zero Dirichlet", "probabilistic"][boundary],
                  nodal_points=n_pts, trees_per_point=a.trees, grid=f"{cfg['n_cells'] + 1}^2",
                  steps=cfg["n_steps"], **ms, wall_ms=wall, max_err=float(d.max()), mean_err=float(d.mean()),
                  reference="single-domain CN/ADI on [-6,6]^2, h=0.05, dt=1e-3 (numpy, %.1f s on the host)" % t_ref)
@@ -56,10 +57,10 @@ def main():
         for r in rows:
             f.write(json.dumps(r) + "\n")
     md = ["# cfg3 PDD (NEXT row f1) on 1 x B200", "",
-          "| outer edges | nodal points x levels | trees/point | T_MC ms | T_INT ms | T_LOCAL ms | wall ms | max err | mean err |",
-          "|---|---|---|---|---|---|---|---|---|"]
+          "| workload | outer edges | nodal points x levels | trees/point | T_MC ms | T_INT ms | T_LOCAL ms | wall ms | max err | mean err |",
+          "|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
-        md.append(f"| {r['boundary']} | {r['nodal_points']} | {r['trees_per_point']:.0e} | {r['T_MC']:.2f} | "
+        md.append(f"| {r['workload']} | {r['boundary']} | {r['nodal_points']} | {r['trees_per_point']:.0e} | {r['T_MC']:.2f} | "
                   f"{r['T_INT']:.3f} | {r['T_LOCAL']:.2f} | {r['wall_ms']:.1f} | {r['max_err']:.2e} | {r['mean_err']:.2e} |")
     md += ["", "Error against " + rows[0]["reference"] + "; grid 81^2 on [-2,2]^2, 500 steps, "
            "nodal lines x = 0, y = 0 (and the four edges) with 17 points x 6 levels."]
