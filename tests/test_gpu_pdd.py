@@ -102,15 +102,17 @@ def test_pdd_exact_data_decoupling(P, reference):
     assert err < 5e-4, err
 
 
-def test_pdd_solve_cfg3_against_reference(P, reference):
+@pytest.mark.parametrize("shared", [0, 1])
+def test_pdd_solve_cfg3_against_reference(P, reference, shared):
     """cfg3's PDD (BASELINE.json configs[2]): nodal values by the tree walk
     (1e6 trees per point and level, probabilistic outer edges), splines, four
     subdomain CN solves, against the single-domain reference.  The nodal
     standard error is <= 0.35/sqrt(1e6) = 3.5e-4; the field is a positive
     weighting of boundary data (maximum principle), so its error stays below
-    the largest nodal error: asserted 2e-3 max, 5e-4 mean."""
+    the largest nodal error: asserted 2e-3 max, 5e-4 mean.  With shared trees
+    (f4) the nodal errors are correlated but each has the same law."""
     x, u = reference
-    eq = W.get("cfg3")["eq"]
+    eq = dict(W.get("cfg3")["eq"], shared=shared)
     cfg = dict(CFG, n_cells=80, n_steps=500, n_trees=1_000_000, seed=7)
     F, V, ms = P.Estimator(eq).pdd_solve(cfg)
     ref = _restrict(x, u, -2.0, 2.0, 80)
