@@ -160,6 +160,39 @@ def oracle_sample(cfg: dict, budget_s: float):
                 sample=f"{n_nodes} nodes x {n_trees} trees of {cfg['name']} (first nodes, first trees)")
 
 
+def _oracle_worker(a):
+    """One single-threaded oracle instance on its own nodes (all-cores baseline)."""
+    import oracle
+    eq, pts, t, n_trees, seed = a
+    t0 = time.perf_counter()
+    _, st = oracle.sums(eq, pts, t, n_trees, seed=seed)
+    return time.perf_counter() - t0, st["trees"], st["leaves"]
+
+
+def oracle_sample_all_cores(cfg: dict, budget_s: float):
+    """The oracle as it stands, one single-threaded instance per host core on
+    disjoint nodes (no change to the oracle itself), sized to ~budget_s."""
+    import multiprocessing as mp
+    import oracle
+    oracle.build()
+    cores = os.cpu_count() or 1
+    eq, t = cfg["eq"], cfg["t"]
+    pts = W.nodes(cfg)
+    t0 = time.perf_counter()
+    oracle.sums(eq, pts[:1], t, 2000, seed=cfg["seed"])
+    per_tree = (time.perf_counter() - t0) / 2000
+    n_trees = max(64, int(budget_s / per_tree))
+    jobs = [(eq, pts[i % len(pts):i % len(pts) + 1], t, n_trees, cfg["seed"]) for i in range(cores)]
+    with mp.get_context("spawn").Pool(cores) as pool:
+        pool.map(_oracle_worker, [(eq, pts[:1], t, 64, cfg["seed"])] * cores)   # start-up, oracle load
+        t0 = time.perf_counter()
+        res = pool.map(_oracle_worker, jobs)
+        wall = time.perf_counter() - t0
+    trees = sum(r[1] for r in res)
+    return dict(seconds=wall, trees=trees, leaves=sum(r[2] for r in res), cores=cores,
+                sample=f"{cores} processes x (1 node x {n_trees} trees) of {cfg['name']}")
+
+
 def run_reference(args, cfg):
     ws, rank, _ = _dist()
     if rank != 0:
@@ -338,6 +371,12 @@ def main():
         r = oracle_sample(cfg, float(os.environ.get("RT_CPU_BASELINE_S", "15")))
         cpu = {"value": r["trees"] / r["seconds"], "unit": "trees/s", "cores": 1, "kind": "oracle",
                "sample": r["sample"], "leaf_evals_per_s": r["leaves"] / r["seconds"]}
+        try:   # the same oracle on every host core (one instance per core)
+            ra = oracle_sample_all_cores(cfg, float(os.environ.get("RT_CPU_BASELINE_S", "15")) / 2)
+            cpu["all_cores"] = {"value": ra["trees"] / ra["seconds"], "cores": ra["cores"],
+                                "sample": ra["sample"]}
+        except Exception as e:   # noqa: BLE001 — a baseline, never fatal
+            cpu["all_cores"] = {"error": str(e)[:200]}
     line = {
         "metric": METRIC, "value": value, "unit": "trees/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
