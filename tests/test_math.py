@@ -1,7 +1,8 @@
 """Accuracy of the product's lean FP64 math (csrc/rt_math.cuh) on the host
 (same source; MUFU seeds emulated in FP32) against 64-bit-mantissa long-double
 references, over the argument domains the tree walk produces.
-The device build is checked the same way in tests/test_gpu_math.py."""
+The device build (real MUFU seeds) is checked the same way in
+tests/test_gpu_math.py."""
 import ctypes as C
 import os
 import subprocess
