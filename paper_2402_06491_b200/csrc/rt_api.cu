@@ -1206,9 +1206,11 @@ extern "C" rt_status rt_fp64_peak(double* out_lane_ops_per_s, double* out_ms) {
   RT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   double* d = nullptr;
   RT_CUDA(cudaMalloc(&d, sizeof(double)));
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+    cudaFree(d);
+    return fail(RT_E_CUDA, "rt_fp64_peak: event creation failed");
+  }
   const int blocks = nsm * 8, threads = 256, iters = 4096;
   fp64_peak_kernel<<<blocks, threads>>>(d, 64, 0.999999, 1e-7);   // warm-up
   cudaEventRecord(e0);

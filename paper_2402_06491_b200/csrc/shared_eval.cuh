@@ -64,8 +64,6 @@ shared_eval_kernel(const __grid_constant__ EvalParams E) {
     if (tid < 32) cnt[tid] = 0;
     __syncthreads();
   }
-  WalkParams G;                                   // g_eval's parameters
-  G.amp = E.amp; G.inv_scale = E.inv_scale; G.inv_scale2 = E.inv_scale2;
   const int64_t j0 = static_cast<int64_t>(blockIdx.y) * E.tpb;
   const int64_t j1 = min(E.M, j0 + E.tpb);
   TreeSum nxt = E.tsum[j0];                       // warp-uniform, prefetched
@@ -95,7 +93,7 @@ shared_eval_kernel(const __grid_constant__ EvalParams E) {
               double xe[DIM];
 #pragma unroll
               for (int k = 0; k < DIM; ++k) xe[k] = x[a][k] + d4[u][k];
-              prod[a] *= g_eval<DIM, GK>(xe, G);
+              prod[a] *= g_eval<DIM, GK>(xe, E.amp, E.inv_scale, E.inv_scale2);
             }
           }
         }

@@ -123,19 +123,27 @@ struct WarpState {
   int gtop, gfree;          // overflow area: bump pointer, free-list size
 };
 
+// The initial data g: constant, tanh step, Gaussian,
+// Lorentzian (the BASELINE.json configs' shapes).
 template <int DIM, int GK>
-__device__ __forceinline__ double g_eval(const double (&x)[DIM], const WalkParams& P) {   // g(x)
+__device__ __forceinline__ double g_eval(const double (&x)[DIM], double amp, double inv_scale,
+                                         double inv_scale2) {
   if constexpr (GK == 0) {
-    return P.amp;
+    return amp;
   } else if constexpr (GK == 1) {
-    return P.amp * 0.5 * (1.0 + tanh(x[0] * P.inv_scale));
+    return amp * 0.5 * (1.0 + tanh(x[0] * inv_scale));
   } else {
     double r2 = x[0] * x[0];
     if constexpr (DIM >= 2) r2 = fma(x[1], x[1], r2);
     if constexpr (DIM >= 3) r2 = fma(x[2], x[2], r2);
-    if constexpr (GK == 2) return P.amp * exp_neg(-r2 * P.inv_scale2);
-    else return P.amp * rcp_nr(fma(r2, P.inv_scale2, 1.0));
+    if constexpr (GK == 2) return amp * exp_neg(-r2 * inv_scale2);
+    else return amp * rcp_nr(fma(r2, inv_scale2, 1.0));
   }
+}
+
+template <int DIM, int GK>
+__device__ __forceinline__ double g_eval(const double (&x)[DIM], const WalkParams& P) {   // g(x)
+  return g_eval<DIM, GK>(x, P.amp, P.inv_scale, P.inv_scale2);
 }
 
 // g in single precision for the FP32-position variant (RT_PREC_FP32_POS):
