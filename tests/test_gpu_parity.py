@@ -517,3 +517,34 @@ def test_extreme_labels_and_depth(P, orc, eq_kw, t, N):
         est.set_pool(pool)
         rec, _ = est.trace(dev(pts), t, N, seed=31)
         assert_trees_equal(rec, orc.trees(eq, pts, t, N, seed=31), eq["K"])
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+def test_cfg5_largest_node_count_sampled(P, orc, fp32):
+    """cfg5's largest node count (BASELINE.json configs[4]: 16384 nodes on
+    [-3, 3], cfg2 equation, t = 1) at 1e6 trees/node: every 2^17-th tree of
+    every node against the oracle (structure bit-exact; C to 1e-12 in FP64,
+    to the FP32-variant bound otherwise), every node counts exactly N, and
+    c_0 matches the heat-kernel closed form e^{-t} A (1+4t)^{-1/2}
+    e^{-x²/(1+4t)} within 4.42 s.e. at the 1024 nodes nearest 0 (R22)."""
+    import closed_forms as cf
+    cfg = W.cfg5(16384, 1_000_000, 1.0, fp32_pos=fp32)
+    eq, N, t = cfg["eq"], cfg["n_trees"], cfg["t"]
+    pts = W.nodes(cfg)
+    est = P.Estimator(eq)
+    rec, sums = est.trace(dev(pts), t, N, seed=cfg["seed"], rec_shift=17)
+    ref = orc.trees_at(dict(eq, precision=0), pts, t, np.arange(0, N, 1 << 17), seed=cfg["seed"])
+    if fp32:
+        assert np.array_equal(rec["ne"], ref["ne"]) and np.array_equal(rec["pruned"], ref["pruned"])
+        keep = ref["pruned"] == 0
+        assert np.array_equal(rec["leaves"][keep], ref["leaves"][keep])
+        assert np.all(np.abs(rec["C"] - ref["C"]) <= 1e-2 * np.abs(ref["C"]) + 1e-30)
+    else:
+        assert_trees_equal(rec, ref, eq["K"])
+    s = sums.cpu().numpy()
+    assert np.all(s[:, :, 2].sum(1) == N)
+    c, se, _, _ = P.finalize(sums, eq["K"], N)
+    mid = np.argsort(np.abs(pts[:, 0]))[:1024]
+    c0, se0 = c[:, 0].cpu().numpy()[mid], se[:, 0].cpu().numpy()[mid]
+    ex = cf.heat(pts[mid], t, eq["D"], 1.0, eq["init_amp"], eq["init_scale"])
+    assert np.max(np.abs((c0 - ex) / se0)) < 4.42
