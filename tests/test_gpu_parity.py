@@ -548,3 +548,25 @@ def test_cfg5_largest_node_count_sampled(P, orc, fp32):
     c0, se0 = c[:, 0].cpu().numpy()[mid], se[:, 0].cpu().numpy()[mid]
     ex = cf.heat(pts[mid], t, eq["D"], 1.0, eq["init_amp"], eq["init_scale"])
     assert np.max(np.abs((c0 - ex) / se0)) < 4.42
+
+
+@pytest.mark.parametrize("name,u0,exact", [
+    ("cfg2", 0.4, 0.17937557929718922),   # u' = f(u), cfg2's f, t = 1
+    ("cfg3", 0.5, 0.35909350167709947),   # cfg2's f, t = 0.5
+    ("cfg4", 0.5, 0.21212126811464993),   # cfg4's f, t = 1
+])
+def test_gpu_constant_data_ode_through_pade(P, name, u0, exact):
+    """Spatially constant data reduce the PDE to u' = f(u) (BASELINE.json
+    north_star): at the configs' full tree counts per node, the CUDA path's
+    [L/M] Padé of the per-order coefficients equals the ODE solution within 4
+    standard errors of the partial sum (R11: the Padé value's delta-method
+    s.e. equals se_sum), at 16 nodes."""
+    cfg = W.get(name)
+    eq = dict(cfg["eq"], init_kind=W.G_CONST, init_amp=u0)
+    pts = W.nodes(cfg)[:16]
+    N = cfg["n_trees"]
+    s = P.Estimator(eq).sums(dev(pts), cfg["t"], N, seed=5)
+    c, se, us, ses = P.finalize(s, eq["K"], N)
+    u, fl = P.pade(c, cfg["L"], cfg["M"])
+    z = (u.cpu().numpy() - exact) / ses.cpu().numpy()
+    assert np.all(np.abs(z) < 4.0), z
