@@ -34,10 +34,27 @@
 // reproducible for a fixed task size, whatever the grid or warp timing.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <type_traits>
 
 #include "philox.cuh"
 #include "rt_math.cuh"
+
+// Debug build (librt_debug.so, -DRT_DEBUG_BOUNDS): device bounds checks on
+// every computed index into the stack pool, free lists, overflow area, ring,
+// shared-tree slots and partials — the GPU pool offers no compute-sanitizer,
+// so the parity tests are re-run against this build (tests/test_gpu_bounds.py).
+#if defined(RT_DEBUG_BOUNDS)
+#define RT_CHECK(c)                                                              \
+  do {                                                                           \
+    if (!(c)) {                                                                  \
+      printf("RT_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);             \
+      __trap();                                                                  \
+    }                                                                            \
+  } while (0)
+#else
+#define RT_CHECK(c) do {} while (0)
+#endif
 
 namespace rtk {
 
@@ -336,6 +353,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     } else {
       flush();
       if (lane < P.nb) {
+        RT_CHECK(task >= 0 && task < P.n_tasks);
         double* o = P.partials + (static_cast<int64_t>(task) * P.nb + lane) * 3;
         o[0] = bsum[lane];
         o[1] = bsum[32 + lane];
@@ -379,6 +397,9 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const unsigned rg = __ballot_sync(0xffffffffu, rel && e >= cap);
     const int gf = ws->gfree;
     __syncwarp();
+    if (rel) RT_CHECK(e >= 0 && e < cap + P.gcap);
+    if (rel && e < cap) RT_CHECK(nfree + __popc(rs & lt_mask) < cap);
+    if (rel && e >= cap) RT_CHECK(gf + __popc(rg & lt_mask) < P.gcap);
     if (rel && e < cap) freeS[nfree + __popc(rs & lt_mask)] = static_cast<uint8_t>(e);
     if (rel && e >= cap) gfl[gf + __popc(rg & lt_mask)] = e - cap;
     nfree += __popc(rs);
@@ -548,6 +569,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     // (before the pops overwrite y): leaves[j][l] = δ of the tree's l-th leaf
     if constexpr (SH) {
       if (active && leaf) {
+        RT_CHECK(leaves < P.lmax && tj - static_cast<uint32_t>(P.tree_offset) < static_cast<uint32_t>(P.n_trees));
         double* const o = P.leaves + (static_cast<int64_t>(tj - static_cast<uint32_t>(P.tree_offset)) *
                                           P.lmax + leaves) * DIM;
 #pragma unroll
@@ -563,7 +585,9 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const int nalc = __popc(alc);
     if (n_glob == 0 && nalc <= nfree) {          // warp-uniform fast path
       if (push) {
+        RT_CHECK(nfree - 1 - __popc(alc & lt_mask) >= 0);
         const int e = freeS[nfree - 1 - __popc(alc & lt_mask)];
+        RT_CHECK(e >= 0 && e < cap);
 #pragma unroll
         for (int q = 0; q < DIM; ++q) pool[q * CAP + e] = static_cast<double>(y[q]);
         pool[DIM * CAP + e] = tau;
@@ -575,6 +599,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       bool last = false;
       if (has) {
 #pragma unroll
+        RT_CHECK(top >= 0 && top < cap);
         for (int q = 0; q < DIM; ++q) y[q] = static_cast<PT>(pool[q * CAP + top]);
         tau = pool[DIM * CAP + top];
         const uint64_t pk = static_cast<uint64_t>(__double_as_longlong(pool[(DIM + 1) * CAP + top]));
@@ -587,6 +612,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       const unsigned rl = __ballot_sync(0xffffffffu, rel);
       __syncwarp();
       if (rel) {
+        RT_CHECK(nfree + __popc(rl & lt_mask) < cap);
         freeS[nfree + __popc(rl & lt_mask)] = static_cast<uint8_t>(top);
         top = prevS[top];
       }
@@ -603,6 +629,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
         } else {
           const int g = rk - nfree;             // g-th overflow entry of this round
           e = cap + (g < gf ? gfl[gf - 1 - g] : gt + (g - gf));
+          RT_CHECK(e - cap < P.gcap);
         }
 #pragma unroll
         for (int q = 0; q < DIM; ++q) *fld(e, q) = static_cast<double>(y[q]);
@@ -668,10 +695,12 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
           ts.bin = pruned ? (P.K + 1) : ne;
           ts.nl = leaves; ts.ne = ne; ts.parts = parts;
           ts.W = pruned ? 0.0 : Pi;
+          RT_CHECK(tj - static_cast<uint32_t>(P.tree_offset) < static_cast<uint32_t>(P.n_trees));
           P.tsum[tj - static_cast<uint32_t>(P.tree_offset)] = ts;
         }
       } else {
         if (done) {
+          RT_CHECK(ring_cnt + rank < kRing);
           ringCode[ring_cnt + rank] = pruned ? (P.K + 1) : ne;
           ringC[ring_cnt + rank] = pruned ? 0.0 : Pi;
         }

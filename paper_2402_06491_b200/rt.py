@@ -14,7 +14,9 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librt.so")
+# RT_LIB_VARIANT=debug selects the bounds-checked build (librt_debug.so, tests only)
+LIB_PATH = os.path.join(_HERE, "librt_debug.so" if os.environ.get("RT_LIB_VARIANT") == "debug"
+                        else "librt.so")
 
 RT_OK, RT_E_ARG, RT_E_CUDA, RT_E_NOMEM, RT_E_STATE = 0, 1, 2, 3, 4
 G_CONST, G_TANH_STEP, G_GAUSS, G_LORENTZ = 0, 1, 2, 3
