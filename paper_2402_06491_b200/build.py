@@ -52,5 +52,13 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
     return so
 
 
+def build_all(force: bool = False) -> None:
+    """The production and the bounds-checked library, compiled concurrently."""
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(2) as ex:
+        for f in [ex.submit(build, force, False, False), ex.submit(build, force, False, True)]:
+            f.result()
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))
