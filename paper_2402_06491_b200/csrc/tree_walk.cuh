@@ -203,6 +203,24 @@ __host__ __device__ constexpr int smem_bytes() {
          9 * 8 + 9 * 4 /* offspring weights and sizes */;
 }
 
+// n += 1 if c, as one predicated add (ptxas otherwise emits add + select)
+__device__ __forceinline__ void inc_if(bool c, int& n) {
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %1, 0;\n\t@p add.s32 %0, %0, 1;\n\t}"
+      : "+r"(n) : "r"(static_cast<int>(c)));
+}
+
+// Ring transposition step: lane b adds record (code, C) to its bin sums iff
+// code == b, as x = (code == b ? C : 0), s1 += x, s2 += x² — one select, no
+// branch (bitwise the conditional sums: s1 is never -0, and 0² leaves s2; the
+// padding records' C is never read into an operand that survives)
+__device__ __forceinline__ void bin_add(int code, int lane, double c, double& s1, double& s2, int& nn) {
+  const bool own = code == lane;
+  const double x = own ? c : 0.0;
+  inc_if(own, nn);
+  s1 += x;
+  s2 = fma(x, x, s2);
+}
+
 // F32 = the FP32-position / FP64-accumulate variant (cfg5, BASELINE.json
 // configs[4]): the clock S, the leaf test, horizons, weights, the tree
 // product and all sums stay FP64 (tree structure identical to the FP64
@@ -307,7 +325,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   uint64_t label = 1;
   int ne = 0, top = -1;                // top: the lane's top stack entry (-1: empty)
   int leaves = 0, parts = 0;           // per-tree counts (trace variant only)
-  uint32_t c_part = 0u, c_leaf = 0u;   // particles / leaves since the last task close
+  int c_part = 0, c_leaf = 0;          // particles / leaves since the last task close
 
   auto start_tree = [&](uint32_t j) {  // a fresh tree j of the current task
     ti = iss_node;
@@ -333,10 +351,10 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       const int4 cd = *reinterpret_cast<const int4*>(ringCode + r);
       const double2 ca = *reinterpret_cast<const double2*>(ringC + r);
       const double2 cb = *reinterpret_cast<const double2*>(ringC + r + 2);
-      if (cd.x == lane) { s1 += ca.x; s2 = fma(ca.x, ca.x, s2); ++nn; }
-      if (cd.y == lane) { s1 += ca.y; s2 = fma(ca.y, ca.y, s2); ++nn; }
-      if (cd.z == lane) { s1 += cb.x; s2 = fma(cb.x, cb.x, s2); ++nn; }
-      if (cd.w == lane) { s1 += cb.y; s2 = fma(cb.y, cb.y, s2); ++nn; }
+      bin_add(cd.x, lane, ca.x, s1, s2, nn);
+      bin_add(cd.y, lane, ca.y, s1, s2, nn);
+      bin_add(cd.z, lane, cb.x, s1, s2, nn);
+      bin_add(cd.w, lane, cb.y, s1, s2, nn);
     }
     ring_cnt = 0;
     bsum[lane] = s1;
@@ -365,7 +383,8 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     }
     // (shared trees: every node sees each walked particle and leaf)
     const unsigned long long scale = SH ? static_cast<unsigned long long>(P.n_points) : 1ull;
-    unsigned long long v0 = c_part * scale, v1 = c_leaf * scale;
+    unsigned long long v0 = static_cast<unsigned long long>(c_part) * scale,
+                       v1 = static_cast<unsigned long long>(c_leaf) * scale;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       v0 += __shfl_xor_sync(0xffffffffu, v0, o);
@@ -375,8 +394,8 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       atomicAdd(P.stats + 2, v0);
       atomicAdd(P.stats + 3, v1);
     }
-    c_part = 0u;
-    c_leaf = 0u;
+    c_part = 0;
+    c_leaf = 0;
     next_task();
     if (!stream_end) {
       const uint32_t take = min(iss_end - iss_next, 32u);
@@ -512,10 +531,12 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     // categorical offspring choice from the integer thresholds (R9)
     // (thresholds past the support are 0xffffffff, so the sum needs no bound)
     const uint32_t c32 = r0.z;
-    int s = (c32 > P.thr[0]) + (c32 > P.thr[1]) + (c32 > P.thr[2]) + (c32 > P.thr[3]);
+    int s = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) inc_if(c32 > P.thr[q], s);
     if (P.n_support > 5) {                      // warp-uniform, rare
 #pragma unroll
-      for (int q = 4; q < 8; ++q) s += (c32 > P.thr[q]) ? 1 : 0;
+      for (int q = 4; q < 8; ++q) inc_if(c32 > P.thr[q], s);
     }
     double gv;                                  // g at the leaf
     if constexpr (F32) gv = static_cast<double>(g_eval_f<DIM, GK>(y, P));
@@ -540,7 +561,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 
     // ---------------- tree logic: predicated straight-line code ---------------
     const bool split = active && !leaf;
-    ne += split ? 1 : 0;                         // splitting events
+    inc_if(split, ne);                           // splitting events
     const bool pruned = split && ne > P.K;       // prune
     const bool kill = split && !pruned && P.n_support == 0;   // purely linear f
     const bool branch = split && !pruned && !kill;
@@ -548,11 +569,11 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const double gl = SH ? 1.0 : gv;            // SH: g is applied per node below
     const double fac = leaf ? (SB ? gl * P.inv_q : gl) : (kill ? 0.0 : wk);
     if (active) Pi *= fac;
-    c_part += active ? 1u : 0u;
-    c_leaf += (active && leaf) ? 1u : 0u;
+    inc_if(active, c_part);
+    inc_if(active && leaf, c_leaf);
     if constexpr (REC || SH) {
-      parts += active ? 1 : 0;
-      if constexpr (!SH) leaves += (active && leaf) ? 1 : 0;   // SH counts at the store below
+      inc_if(active, parts);
+      if constexpr (!SH) inc_if(active && leaf, leaves);   // SH counts at the store below
     }
     const bool push = branch && k > 1;           // k-1 younger siblings wait
     const bool pop = (active && leaf) || (branch && k == 0);
@@ -680,11 +701,25 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     if (fin != 0u) {
       // a pruned tree aborts with groups still pending: return its entries
       bool drain = done && top >= 0;
-      while (__any_sync(0xffffffffu, drain)) {
-        const int e = top;
-        if (drain) top = prev_of(top);
-        release_generic(drain, e);
-        drain = drain && top >= 0;
+      if (n_glob == 0) {                         // warp-uniform: shared entries only
+        while (__any_sync(0xffffffffu, drain)) {
+          const unsigned rs = __ballot_sync(0xffffffffu, drain);
+          if (drain) {
+            RT_CHECK(top >= 0 && top < cap && nfree + __popc(rs & lt_mask) < cap);
+            freeS[nfree + __popc(rs & lt_mask)] = static_cast<uint8_t>(top);
+            top = prevS[top];
+          }
+          nfree += __popc(rs);
+          drain = drain && top >= 0;
+        }
+        __syncwarp();
+      } else {
+        while (__any_sync(0xffffffffu, drain)) {
+          const int e = top;
+          if (drain) top = prev_of(top);
+          release_generic(drain, e);
+          drain = drain && top >= 0;
+        }
       }
       const int nfin = __popc(fin);
       const int rank = __popc(fin & lt_mask);
