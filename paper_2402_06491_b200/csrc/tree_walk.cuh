@@ -138,6 +138,8 @@ __device__ __forceinline__ unsigned long long global_ns() {
 struct WarpState {
   double iss_y[3];          // coordinates of the current task's node
   int gtop, gfree;          // overflow area: bump pointer, free-list size
+  double* gpool;            // the warp's overflow area (read in the slow paths only,
+  int* gprev;               //   so the compiler does not keep or rematerialise them)
 };
 
 // The initial data g: constant, tanh step, Gaussian,
@@ -272,9 +274,16 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 
   const int gwarp = blockIdx.x * kWarpsPerCta + wib;
   if (P.wtime != nullptr && lane == 0) P.wtime[4 * gwarp] = global_ns();
-  double* const gpool = P.gpool + static_cast<int64_t>(gwarp) * P.gcap * NF;
-  int* const gprev = P.gaux + static_cast<int64_t>(gwarp) * 2 * P.gcap;
-  int* const gfl = gprev + P.gcap;
+  if (lane == 0) {
+    ws->gpool = P.gpool + static_cast<int64_t>(gwarp) * P.gcap * NF;
+    ws->gprev = P.gaux + static_cast<int64_t>(gwarp) * 2 * P.gcap;
+  }
+  __syncwarp();
+  // overflow-area bases, re-read from shared memory where used (volatile: no
+  // hoisting into the fast path)
+  auto gpool = [&]() -> double* { return *static_cast<double* volatile*>(&ws->gpool); };
+  auto gprev = [&]() -> int* { return *static_cast<int* volatile*>(&ws->gprev); };
+  auto gfl = [&]() -> int* { return gprev() + P.gcap; };
 
   // ---- warp-uniform stream state -------------------------------------------
   // The warp fetches tasks dynamically (one atomicAdd per task) and runs each
@@ -407,9 +416,9 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   // ---- stack-pool slow path (overflow entries in global memory) -----------
   // entry e < cap lives in shared memory, e >= cap at gpool[e - cap]
   auto fld = [&](int e, int f) -> double* {
-    return e < cap ? pool + f * CAP + e : gpool + static_cast<int64_t>(e - cap) * NF + f;
+    return e < cap ? pool + f * CAP + e : gpool() + static_cast<int64_t>(e - cap) * NF + f;
   };
-  auto prev_of = [&](int e) -> int { return e < cap ? static_cast<int>(prevS[e]) : gprev[e - cap]; };
+  auto prev_of = [&](int e) -> int { return e < cap ? static_cast<int>(prevS[e]) : gprev()[e - cap]; };
   // return entry e of every lane with rel set to the free lists
   auto release_generic = [&](bool rel, int e) {
     const unsigned rs = __ballot_sync(0xffffffffu, rel && e < cap);
@@ -420,7 +429,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     if (rel && e < cap) RT_CHECK(nfree + __popc(rs & lt_mask) < cap);
     if (rel && e >= cap) RT_CHECK(gf + __popc(rg & lt_mask) < P.gcap);
     if (rel && e < cap) freeS[nfree + __popc(rs & lt_mask)] = static_cast<uint8_t>(e);
-    if (rel && e >= cap) gfl[gf + __popc(rg & lt_mask)] = e - cap;
+    if (rel && e >= cap) gfl()[gf + __popc(rg & lt_mask)] = e - cap;
     nfree += __popc(rs);
     n_glob -= __popc(rg);
     if (lane == 0) ws->gfree = gf + __popc(rg);
@@ -649,7 +658,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
           e = freeS[nfree - 1 - rk];
         } else {
           const int g = rk - nfree;             // g-th overflow entry of this round
-          e = cap + (g < gf ? gfl[gf - 1 - g] : gt + (g - gf));
+          e = cap + (g < gf ? gfl()[gf - 1 - g] : gt + (g - gf));
           RT_CHECK(e - cap < P.gcap);
         }
 #pragma unroll
@@ -657,7 +666,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
         *fld(e, DIM) = tau;
         *fld(e, DIM + 1) = __longlong_as_double(static_cast<long long>(push_pk));
         if (e < cap) prevS[e] = static_cast<int16_t>(top);
-        else gprev[e - cap] = top;
+        else gprev()[e - cap] = top;
         top = e;
       }
       const int ng = max(0, nalc - nfree);
@@ -736,7 +745,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       } else {
         if (done) {
           RT_CHECK(ring_cnt + rank < kRing);
-          ringCode[ring_cnt + rank] = pruned ? (P.K + 1) : ne;
+          ringCode[ring_cnt + rank] = ne;             // = K+1 (the pruned bin) iff pruned
           ringC[ring_cnt + rank] = pruned ? 0.0 : Pi;
         }
         ring_cnt += nfin;
