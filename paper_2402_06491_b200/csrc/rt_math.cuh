@@ -90,11 +90,14 @@ RTM_HD double fma_d(double a, double b, double c) {
 // logc = -log(invc); r = z·invc − 1 (one rounding, |r| <= 2^-7);
 // log x = k ln2 + logc + r + r²·P(r).  11 FP64 ops + 1 I2F.
 RTM_HD double log_tab(double x, const LogEntry* T) {
+  // (all on the high word: bits(0.6875) has a zero low word, so the 64-bit
+  // difference never borrows and z keeps x's low word)
   const uint64_t ix = dbits(x);
-  const uint64_t tmp = ix - kLogOff;
-  const int i = static_cast<int>((tmp >> 45) & 127u);
-  const int64_t k = static_cast<int64_t>(tmp) >> 52;
-  const double z = dfrom(ix - (tmp & (0xfffull << 52)));
+  const uint32_t hi = static_cast<uint32_t>(ix >> 32);
+  const uint32_t tmp = hi - static_cast<uint32_t>(kLogOff >> 32);
+  const int i = static_cast<int>((tmp >> 13) & 127u);
+  const int k = static_cast<int32_t>(tmp) >> 20;
+  const double z = dfrom((static_cast<uint64_t>(hi - (tmp & 0xfff00000u)) << 32) | (ix & 0xffffffffull));
   const LogEntry e = T[i];
   const double r = fma_d(z, e.invc, -1.0);
   double p = kLogP[6];
@@ -169,6 +172,68 @@ RTM_HD double cospi2(double a) {
   p = fma_d(p, f2, kCosPiW[1]);
   p = fma_d(p, f2, kCosPiW[0]);
   const uint64_t neg = (static_cast<uint64_t>(static_cast<int>(n)) & 1ull) << 63;
+  return dfrom(dbits(p) ^ neg);
+}
+
+// The angles of the d = 3 Box–Muller draws, 2π·v with v = (2w+1)·2^-33 the
+// 32-bit uniform of word w, reduced on the integer instead of in FP64 —
+// bitwise the same q and f as sincospi2(2v) / cospi2(2v):
+//   sincospi2: 2·(2v) = (w + 1/2)·2^-30, q = rint = ((w >> 29) + 1) >> 1,
+//              f = 2v − q/2 = ((2w+1) − q·2^31)·2^-32, |f| <= 1/4;
+//   cospi2:    2v = (w + 1/2)·2^-31, n = rint = ((w >> 30) + 1) >> 1,
+//              f = 2v − n = ((2w+1) − n·2^32)·2^-32, |f| < 1/2;
+// the differences d are odd and fit an int32, so they are the wrapped uint32
+// differences reinterpreted.  The polynomials are evaluated in d itself with
+// the coefficients pre-scaled by exact powers of two (k_n 2^(-64n), sin also
+// 2^-32): Horner in d·d = 2^64 f·f then gives the same bits as in f·f.
+RTM_HD void sincos2pi_u32(uint32_t w, double& s_out, double& c_out) {
+  const uint32_t q = ((w >> 29) + 1u) >> 1;
+  const double d = static_cast<double>(static_cast<int32_t>(2u * w + 1u - (q << 31)));
+  const double D = d * d;
+  double ps = kSinPi32[7];
+  ps = fma_d(ps, D, kSinPi32[6]);
+  ps = fma_d(ps, D, kSinPi32[5]);
+  ps = fma_d(ps, D, kSinPi32[4]);
+  ps = fma_d(ps, D, kSinPi32[3]);
+  ps = fma_d(ps, D, kSinPi32[2]);
+  ps = fma_d(ps, D, kSinPi32[1]);
+  ps = fma_d(ps, D, kSinPi32[0]);
+  double pc = kCosPi32[8];
+  pc = fma_d(pc, D, kCosPi32[7]);
+  pc = fma_d(pc, D, kCosPi32[6]);
+  pc = fma_d(pc, D, kCosPi32[5]);
+  pc = fma_d(pc, D, kCosPi32[4]);
+  pc = fma_d(pc, D, kCosPi32[3]);
+  pc = fma_d(pc, D, kCosPi32[2]);
+  pc = fma_d(pc, D, kCosPi32[1]);
+  const double s = ps * d;
+  const double c = fma_d(pc, D, kCosPi32[0]);
+  const int qi = static_cast<int>(q) & 3;
+  const bool swap = qi & 1;
+  double so = swap ? c : s;
+  double co = swap ? s : c;
+  const uint64_t sneg = (qi & 2) ? 0x8000000000000000ull : 0ull;
+  const uint64_t cneg = ((qi + 1) & 2) ? 0x8000000000000000ull : 0ull;
+  s_out = dfrom(dbits(so) ^ sneg);
+  c_out = dfrom(dbits(co) ^ cneg);
+}
+
+RTM_HD double cos2pi_u32(uint32_t w) {
+  const double d = static_cast<double>(static_cast<int32_t>(2u * w + 1u));
+  const double D = d * d;
+  double p = kCosPiW32[11];
+  p = fma_d(p, D, kCosPiW32[10]);
+  p = fma_d(p, D, kCosPiW32[9]);
+  p = fma_d(p, D, kCosPiW32[8]);
+  p = fma_d(p, D, kCosPiW32[7]);
+  p = fma_d(p, D, kCosPiW32[6]);
+  p = fma_d(p, D, kCosPiW32[5]);
+  p = fma_d(p, D, kCosPiW32[4]);
+  p = fma_d(p, D, kCosPiW32[3]);
+  p = fma_d(p, D, kCosPiW32[2]);
+  p = fma_d(p, D, kCosPiW32[1]);
+  p = fma_d(p, D, kCosPiW32[0]);
+  const uint64_t neg = static_cast<uint64_t>(((w >> 30) + 1u) & 2u) << 62;   // n odd
   return dfrom(dbits(p) ^ neg);
 }
 

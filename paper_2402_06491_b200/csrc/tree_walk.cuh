@@ -519,23 +519,23 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       // the word of the 12 low bits the 53-bit uniforms leave unused
       const double v1 = unif53(r1.x, r1.y);
       const double v3 = unif53(r1.z, r1.w);
-      double v2, v4;
+      // (angles 2π·unif32(w), reduced on the integer word: rt_math.cuh)
+      uint32_t w2, w4;
       if constexpr (SB) {                        // block-0 word 3 is ξ: angles from block 2
         const uint4 r2 = philox4x32_10(tj, c1, c2, c3 | (2u << 24), P.rk);
-        v2 = unif32(r2.x);
-        v4 = unif32(r2.y);
+        w2 = r2.x;
+        w4 = r2.y;
       } else {
-        const uint32_t w4 = ((r0.x & 0xFFFu) << 20) | ((r1.x & 0xFFFu) << 8) | ((r1.z & 0xFFFu) >> 4);
-        v2 = unif32(r0.w);
-        v4 = unif32(w4);
+        w4 = ((r0.x & 0xFFFu) << 20) | ((r1.x & 0xFFFu) << 8) | ((r1.z & 0xFFFu) >> 4);
+        w2 = r0.w;
       }
       const double rad = sqrt_nr(-2.0 * log_tab(v1, ltab) * h2d);
       double sn, cs;
-      sincospi2(2.0 * v2, sn, cs);
+      sincos2pi_u32(w2, sn, cs);
       y[0] = fma(rad, cs, y[0]);
       y[1] = fma(rad, sn, y[1]);
       const double rad2 = sqrt_nr(-2.0 * log_tab(v3, ltab) * h2d);
-      y[2] = fma(rad2, cospi2(2.0 * v4), y[2]);
+      y[2] = fma(rad2, cos2pi_u32(w4), y[2]);
     }
     // categorical offspring choice from the integer thresholds (R9)
     // (thresholds past the support are 0xffffffff, so the sum needs no bound)

@@ -16,6 +16,8 @@ __global__ void math_kernel(int which, const double* x, long n, double* y, doubl
     case 2: y[q] = cospi2(x[q]); break;
     case 3: y[q] = sqrt_nr(x[q]); break;
     case 4: y[q] = rcp_nr(x[q]); break;
+    case 6: sincos2pi_u32(static_cast<uint32_t>(x[q]), y[q], z[q]); break;
+    case 7: y[q] = cos2pi_u32(static_cast<uint32_t>(x[q])); break;
     default: y[q] = exp_neg(x[q]); break;
   }
 }

@@ -68,3 +68,19 @@ def test_device_sqrt_rcp_exp(dev):
     v, _ = _run(dev, 5, e)
     ref = np.exp(e.astype(np.longdouble))
     assert float(np.max(np.abs(v - ref) / ref)) < 4 * EPS
+
+
+def test_device_u32_angles_bitwise(dev):
+    """The integer-reduced d = 3 angles equal the FP64-reduced ones bit for bit
+    on the device too (tests/test_math.py does the host build)."""
+    e = [k * 2 ** 29 + d for k in range(9) for d in (-2, -1, 0, 1) if 0 <= k * 2 ** 29 + d < 2 ** 32]
+    w = np.concatenate([np.array(e, dtype=np.float64),
+                        np.random.default_rng(12).integers(0, 2 ** 32, 400_000).astype(np.float64)])
+    a = 2.0 * (2 * w + 1) * 2.0 ** -33
+    s_ref, c_ref = _run(dev, 1, a)
+    s, c = _run(dev, 6, w)
+    assert np.array_equal(s.view(np.uint64), s_ref.view(np.uint64))
+    assert np.array_equal(c.view(np.uint64), c_ref.view(np.uint64))
+    c1, _ = _run(dev, 2, a)
+    c2, _ = _run(dev, 7, w)
+    assert np.array_equal(c2.view(np.uint64), c1.view(np.uint64))

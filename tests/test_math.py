@@ -93,6 +93,40 @@ def test_cospi2_single_polynomial(m):
     assert got[-11] == 1.0 and got[-9] == -1.0 and got[-7] == 1.0
 
 
+def _w_edges():
+    """32-bit words around every reduction boundary (quadrant / half-turn
+    edges at multiples of 2^29) plus random ones."""
+    e = []
+    for k in range(9):
+        for d in (-2, -1, 0, 1):
+            v = k * 2 ** 29 + d
+            if 0 <= v < 2 ** 32:
+                e.append(v)
+    r = np.random.default_rng(11).integers(0, 2 ** 32, size=500_000, dtype=np.uint64)
+    return np.concatenate([np.array(e, dtype=np.uint64), r]).astype(np.uint32)
+
+
+def test_u32_angle_reductions_bitwise(m):
+    """sincos2pi_u32(w) / cos2pi_u32(w) (the integer reduction of the d = 3
+    angles) equal sincospi2(2v) / cospi2(2v) bit for bit, v = (2w+1)·2^-33
+    (the FP64 reduction they replace: same q, same exact f)."""
+    w = _w_edges()
+    a = 2.0 * (2 * w.astype(np.float64) + 1) * 2.0 ** -33
+    assert np.array_equal((2 * w.astype(np.uint64) + 1).astype(np.float64), 2 * w.astype(np.float64) + 1)
+    s_ref = np.empty_like(a); c_ref = np.empty_like(a)
+    m.m_sincospi2(a.ctypes.data, a.size, s_ref.ctypes.data, c_ref.ctypes.data)
+    s = np.empty_like(a); c = np.empty_like(a)
+    m.m_sincos2pi_u32.argtypes = [C.c_void_p, C.c_long, C.c_void_p, C.c_void_p]
+    m.m_sincos2pi_u32(w.ctypes.data, w.size, s.ctypes.data, c.ctypes.data)
+    assert np.array_equal(s.view(np.uint64), s_ref.view(np.uint64))
+    assert np.array_equal(c.view(np.uint64), c_ref.view(np.uint64))
+    c1 = _call(m, "m_cospi2", a)
+    c2 = np.empty_like(a)
+    m.m_cos2pi_u32.argtypes = [C.c_void_p, C.c_long, C.c_void_p]
+    m.m_cos2pi_u32(w.ctypes.data, w.size, c2.ctypes.data)
+    assert np.array_equal(c2.view(np.uint64), c1.view(np.uint64))
+
+
 def test_sqrt_rcp(m):
     rng = np.random.default_rng(4)
     x = np.concatenate([np.exp(rng.uniform(-80, 80, 300_000)), [0.0, 1.0, 4.0, 2.0 ** -60]])
