@@ -78,11 +78,17 @@ def algo_fp64_per_unit(eq: dict) -> dict:
                 tree=3 + (1 if strat == 1 else 0))       # C², ΣC, ΣC² (× e^{λt})
 
 
-def algo_fp64_ops(eq: dict, stats: dict) -> float:
-    """Algorithmic FP64 lane-ops of one launch from its event counters."""
+def algo_fp64_ops(eq: dict, stats: dict, n_points: int = 1) -> float:
+    """Algorithmic FP64 lane-ops of one launch from its event counters.
+
+    Shared trees (f4): the statistics count per (node, tree), but the method
+    walks each tree once for all n_points nodes — particles and splits are
+    credited once per tree; the g evaluations (leaves) and the per-tree
+    accumulation happen per node."""
     u = algo_fp64_per_unit(eq)
-    return (stats["particles"] * u["particle"] + stats["leaves"] * u["leaf"] +
-            stats["splits"] * u["split"] + stats["trees"] * u["tree"])
+    walk = 1.0 / n_points if eq.get("shared") else 1.0
+    return (stats["particles"] * walk * u["particle"] + stats["leaves"] * u["leaf"] +
+            stats["splits"] * walk * u["split"] + stats["trees"] * u["tree"])
 
 
 class ClockSampler:
@@ -313,7 +319,7 @@ def main():
     trees_all = n * N * ws * args.steps
     value = trees_all / (tot_ms / 1e3)
     leaves_all = st_one["leaves"] * ws * args.steps
-    ops = algo_fp64_ops(eq, st_one)
+    ops = algo_fp64_ops(eq, st_one, n)
     peak = N_SM * FP64_LANES * F_MAX_MHZ * 1e6 / 1e12       # T lane-ops/s
     achieved = ops / (walk_avg / 1e3) / 1e12
     clocks = clk.summary()

@@ -44,13 +44,7 @@ def main():
             st = est.stats()
             ms.append(st["kernel_ms"])
         kms = min(ms)
-        st_ops = dict(st)
-        if eq.get("shared"):
-            # shared trees: each 32-node tile walks the trees once; every node
-            # evaluates g at every leaf (stats count per node-tree)
-            tiles = (n + 31) // 32
-            for k in ("particles", "splits", "trees"):
-                st_ops[k] = st[k] * tiles / n
+        st_ops = dict(st)   # (shared trees: the walk is credited once per tree, bench.algo_fp64_ops)
         c, se = est.estimate(x, t, N, cfg["seed"])
         u, fl = P.pade(c, cfg["L"], cfg["M"])
         r = dict(workload=name, strategy=["potential", "A_shift", "B"][eq.get("strategy", 0)]
@@ -60,7 +54,7 @@ def main():
                  leaf_evals_per_s=st["leaves"] / (kms / 1e3),
                  particles_per_tree=st["particles"] / st["trees"],
                  pruned_fraction=st["pruned"] / st["trees"],
-                 fp64_roofline_frac=bench.algo_fp64_ops(eq, st_ops) / (kms / 1e3) / peak,
+                 fp64_roofline_frac=bench.algo_fp64_ops(eq, st_ops, n) / (kms / 1e3) / peak,
                  u_mid=float(u[n // 2].item()))
         rows.append(r)
         print(json.dumps(r), flush=True)
