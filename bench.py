@@ -37,45 +37,48 @@ import workloads as W  # noqa: E402
 # (MEASURED_PEAKS.json sm_max_mhz; /opt/skills/guides/B200_PROFILING.md).
 N_SM, FP64_LANES, F_MAX_MHZ = 148, 64, 1965.0
 
-# Algorithmic FP64 work: the method written plainly — as the
-# oracle does, S = -log(U)/λ, x' = y + σ sqrt(h) ξ with textbook Box–Muller —
-# costed with the FP64-pipe instructions CUDA's own libdevice routines issue
-# on their main path (tools/libdevice_costs.py: CUDA 12.9, sm_100a), plus one
-# per plain add/mul/fma/compare.  The kernel's own cheaper math therefore
-# raises the achieved rate; it cannot inflate the count.
-LD = dict(log=30, exp=18, sqrt=8, div=8, tanh=37, sincospi=25, cospi=16, u2d=1)
+# Algorithmic FP64 work: SURVEY.md §8(d)'s per-unit figure —
+# what the method itself must compute, costed with SURVEY's fixed table
+# (FP64 ops: log 20, exp 15, sincospi 20, sqrt 8, div 8, tanh 25;
+# fma/mul/add/compare 1) — times the units one launch processes (its event
+# counters).  Per particle: one exponential variate (1 log), ⌈d/2⌉ Box–Muller
+# pairs (each 1 log + 1 sqrt + 1 sincospi), 1 sqrt, d FMA + 1 sub + 1 compare
+# + 1 mul; per leaf: g (its argument, the transcendental or reciprocal, the
+# amplitude) + 1 mul; per split: 1 mul; per tree: 1 mul + 2 adds.  The
+# kernel's own cheaper math raises the achieved rate; it cannot inflate the
+# count.  (An earlier table costed each routine with CUDA libdevice's own
+# SASS — log 30, exp 18, sincospi 25, tanh 37 — and read 0.61 at cfg4.)
+SV = dict(log=20, exp=15, sqrt=8, div=8, tanh=25, sincospi=20)
 
 
 def algo_fp64_per_unit(eq: dict) -> dict:
     d = eq["dim"]
     strat = eq.get("strategy", 0)
-    unif = LD["u2d"] + 1                                   # (double)m * 2^-53
-    pair_both = 2 * unif + LD["log"] + 1 + LD["sqrt"] + 1 + LD["sincospi"] + 2
-    pair_cos = 2 * unif + LD["log"] + 1 + LD["sqrt"] + 1 + LD["cospi"] + 1
+    pairs = (d + 1) // 2
     if strat == 2:                                         # Strategy B: ξ integer test,
-        clock = unif + 3                                   # h = τS, τ_c = τ(1 - S)
+        clock = 2                                          # h = τS, τ_c = τ(1 - S)
     else:
-        clock = unif + LD["log"] + 1 + 1                   # S = -log(U)/λ, S > τ
+        clock = SV["log"]                                  # S = -log(U)/λ
     per_particle = (clock
-                    + LD["sqrt"] + 1             # σ sqrt(h)
-                    + d)                         # y_k + (σ√h) ξ_k
-    per_particle += {1: pair_cos, 2: pair_both, 3: pair_both + pair_cos}[d]
+                    + pairs * (SV["log"] + SV["sqrt"] + SV["sincospi"])
+                    + SV["sqrt"]                           # σ sqrt(h)
+                    + d + 3)                               # y_k + (σ√h) ξ_k, τ - S, S > τ, 2D h
     r2 = 2 * d - 1
     g = {W.G_CONST: 0,
-         W.G_TANH_STEP: LD["div"] + LD["tanh"] + 1 + 2,
-         W.G_GAUSS: r2 + LD["div"] + LD["exp"] + 1,
-         W.G_LORENTZ: r2 + LD["div"] + 1 + LD["div"]}[eq["init_kind"]]
-    split = 2                                            # Π *= w_k, τ_c
+         W.G_TANH_STEP: 1 + SV["tanh"] + 2,                # x/s, tanh, amp (1 + ·)/2
+         W.G_GAUSS: r2 + 1 + SV["exp"] + 1,                # |x|², /s², exp, amp
+         W.G_LORENTZ: r2 + 1 + 1 + SV["div"] + 1}[eq["init_kind"]]   # |x|², /s², 1 +, 1/·, amp
+    split = 1                                              # Π *= w_k
     if strat == 1:
-        split += LD["exp"] + 2                           # e^{(k-1)λτ_c}
+        split += SV["exp"] + 2                             # e^{(k-1)λτ_c}
     if strat == 2:
-        split += 1                                       # η(τ) = τ
+        split += 1                                         # η(τ) = τ
     if any(eq.get("coef_kind", [0] * 9)):
-        split += LD["exp"] + LD["div"] + 4               # e^{-y²/s²}/(τ_c + t0)
+        split += SV["exp"] + SV["div"] + 4                 # e^{-y²/s²}/(τ_c + t0)
     return dict(particle=per_particle,
-                leaf=g + 1 + (1 if strat == 2 else 0),   # Π *= g (/ q)
+                leaf=g + 1 + (1 if strat == 2 else 0),     # Π *= g (/ q)
                 split=split,
-                tree=3 + (1 if strat == 1 else 0))       # C², ΣC, ΣC² (× e^{λt})
+                tree=3 + (1 if strat == 1 else 0))         # ΣC += C, ΣC² += C·C (× e^{λt})
 
 
 def algo_fp64_ops(eq: dict, stats: dict, n_points: int = 1) -> float:

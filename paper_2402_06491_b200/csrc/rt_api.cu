@@ -88,7 +88,7 @@ struct rt_handle {
   cudaStream_t last_stream = nullptr;
   bool have_timing = false;
   double host_total_ms = -1.0;
-  DevBuf partials, gpool, gaux, wtime, sh_tsum, sh_leaves, pdd_pts, pdd_nodal, pdd_bc, pdd_field, pdd_c, pdd_u, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
+  DevBuf partials, gpool, gaux, wtime, sh_tsum, sh_leaves, sh_sorted, sh_boff, pdd_pts, pdd_nodal, pdd_bc, pdd_field, pdd_c, pdd_u, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
   int32_t grid_override = 0;
   int64_t tpt_override = 0;
   int32_t pool_override = 0;
@@ -224,7 +224,7 @@ extern "C" rt_status rt_destroy(rt_handle* h) {
   if (!h) return RT_OK;
   if (h->own_stream) cudaStreamSynchronize(h->own_stream);
   if (h->last_stream) cudaStreamSynchronize(h->last_stream);
-  for (DevBuf* b : {&h->partials, &h->gpool, &h->gaux, &h->wtime, &h->sh_tsum, &h->sh_leaves, &h->pdd_pts, &h->pdd_nodal,
+  for (DevBuf* b : {&h->partials, &h->gpool, &h->gaux, &h->wtime, &h->sh_tsum, &h->sh_leaves, &h->sh_sorted, &h->sh_boff, &h->pdd_pts, &h->pdd_nodal,
                     &h->pdd_bc, &h->pdd_field, &h->pdd_c, &h->pdd_u, &h->sums, &h->stats, &h->h_points, &h->h_coeffs,
                     &h->h_stderr, &h->h_aux, &h->h_flags})
     b->release();
@@ -474,29 +474,35 @@ static rt_status run_walk_shared(rt_handle* h, KernelFn prod, int smem, int pool
   const int64_t M = std::max<int64_t>(1, std::min<int64_t>(n_trees, static_cast<int64_t>(4.0e9 / per_tree)));
   const int64_t n_chunks = (n_trees + M - 1) / M;
   // phase 2 geometry: 64 or 128 nodes (1 or 2 per thread) x tpb trees per
-  // CTA, enough CTAs for the GPU
+  // CTA; about four waves of resident CTAs per chunk (the last wave's tail
+  // is then a small share)
   const int npt = n_points >= 256 ? 2 : 1;
   const int npc = rtk::kEvalThreads * npt;
   const int tiles = static_cast<int>((n_points + npc - 1) / npc);
-  int64_t tpb = M / std::max<int64_t>(1, (148 * 16 + tiles - 1) / tiles);
+  KernelFn ev = nullptr, evr = nullptr;
+#define RT_E(D, G) if (p.dim == D && p.init_kind == G) { ev = eval_kernel<D, G, false>(npt); evr = eval_kernel<D, G, true>(npt); }
+  RT_E(1, 0) RT_E(1, 1) RT_E(1, 2) RT_E(1, 3) RT_E(2, 0) RT_E(2, 1) RT_E(2, 2) RT_E(2, 3)
+  RT_E(3, 0) RT_E(3, 1) RT_E(3, 2) RT_E(3, 3)
+#undef RT_E
+  // (148 = B200's SM count as a constant, not the device's: the tree blocks
+  // fix the summation order, which must not depend on the GPU it runs on)
+  int ev_per_sm = 0;
+  RT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ev_per_sm, (const void*)ev, rtk::kEvalThreads, 0));
+  const int64_t want_blocks = std::max<int64_t>(1, (int64_t(4) * 148 * std::max(1, ev_per_sm) + tiles - 1) / tiles);
+  int64_t tpb = (M + want_blocks - 1) / want_blocks;
   tpb = std::max<int64_t>(128, std::min<int64_t>(tpb, 8192));
   int64_t tpn_total = 0;
   for (int64_t c = 0; c < n_chunks; ++c) tpn_total += (std::min(M, n_trees - c * M) + tpb - 1) / tpb;
   RT_CUDA(h->partials.ensure(static_cast<size_t>(n_points) * tpn_total * nb * 3 * sizeof(double)));
   RT_CUDA(h->sh_tsum.ensure(static_cast<size_t>(M) * sizeof(rtk::TreeSum)));
   RT_CUDA(h->sh_leaves.ensure(static_cast<size_t>(M) * lmax * d * sizeof(double)));
+  RT_CUDA(h->sh_sorted.ensure(static_cast<size_t>(M) * sizeof(rtk::TreeSum)));
+  RT_CUDA(h->sh_boff.ensure(static_cast<size_t>((M + tpb - 1) / tpb) * (nb + 1) * sizeof(int32_t)));
   const int gcap = 32 * (p.K + 1);
   const size_t nwarps = static_cast<size_t>(grid) * rtk::kWarpsPerCta;
   RT_CUDA(h->gpool.ensure(nwarps * gcap * nf * sizeof(double)));
   RT_CUDA(h->gaux.ensure(nwarps * 2 * gcap * sizeof(int32_t)));
   if (h->pool_override > 0) pool_cap = std::min(pool_cap, static_cast<int>(h->pool_override));
-  KernelFn ev = nullptr, evr = nullptr;
-#define RT_E(D, G) if (p.dim == D && p.init_kind == G) { ev = eval_kernel<D, G, false>(npt); evr = eval_kernel<D, G, true>(npt); }
-  RT_E(1, 0) RT_E(1, 1) RT_E(1, 2) RT_E(1, 3) RT_E(2, 0) RT_E(2, 1) RT_E(2, 2) RT_E(2, 3)
-  RT_E(3, 0) RT_E(3, 1) RT_E(3, 2) RT_E(3, 3)
-#undef RT_E
-  const int esmem = nb * 2 * rtk::kEvalThreads * npt * 8;
-  RT_CUDA(cudaFuncSetAttribute((const void*)ev, cudaFuncAttributeMaxDynamicSharedMemorySize, esmem));
 
   WalkParams P;
   fill_params(h, P, t, seed);
@@ -519,6 +525,8 @@ static rt_status run_walk_shared(rt_handle* h, KernelFn prod, int smem, int pool
   E.partials = static_cast<double*>(h->partials.p); E.tpn_total = tpn_total;
   E.recs = d_recs; E.rec_shift = rec_shift;
   E.n_rec = (n_trees + (int64_t(1) << rec_shift) - 1) >> rec_shift;
+  E.sorted = static_cast<rtk::TreeSum*>(h->sh_sorted.p);
+  E.boff = static_cast<int32_t*>(h->sh_boff.p);
 
   RT_CUDA(cudaMemsetAsync(h->stats.p, 0, 6 * sizeof(unsigned long long), st));
   RT_CUDA(cudaEventRecord(h->ev[0], st));
@@ -541,7 +549,9 @@ static rt_status run_walk_shared(rt_handle* h, KernelFn prod, int smem, int pool
     E.q0 = q0;
     E.rel0 = static_cast<uint32_t>(c * M);
     const dim3 eg(static_cast<unsigned>(tiles), static_cast<unsigned>((Mc + tpb - 1) / tpb));
-    reinterpret_cast<void (*)(rtk::EvalParams)>(ev)<<<eg, rtk::kEvalThreads, esmem, st>>>(E);
+    rtk::bin_sort_kernel<<<eg.y, 32, 0, st>>>(E);
+    RT_CUDA(cudaGetLastError());
+    reinterpret_cast<void (*)(rtk::EvalParams)>(ev)<<<eg, rtk::kEvalThreads, 0, st>>>(E);
     RT_CUDA(cudaGetLastError());
     if (d_recs) {
       reinterpret_cast<void (*)(rtk::EvalParams)>(evr)<<<eg, rtk::kEvalThreads, 0, st>>>(E);

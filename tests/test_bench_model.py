@@ -11,14 +11,17 @@ import workloads as W  # noqa: E402
 
 
 def test_cost_model_per_unit_counts():
-    """Per-unit costs follow the libdevice table: d = 3 draws one more cosine
-    normal than d = 2, which draws one sin/cos pair more than d = 1's cosine."""
+    """Per-unit costs are SURVEY.md §8(d)'s list: one exponential variate,
+    ⌈d/2⌉ Box–Muller pairs, one sqrt, d + 3 plain ops per particle."""
     u1 = bench.algo_fp64_per_unit(W.get("cfg2")["eq"])
     u3 = bench.algo_fp64_per_unit(W.get("cfg4")["eq"])
-    assert u1["particle"] < u3["particle"]
-    assert u3["tree"] == 3 and u1["split"] == 2
-    # Lorentzian g (cfg4): r² (2d-1 ops) + two divisions + the product
-    assert u3["leaf"] == 5 + 2 * bench.LD["div"] + 1 + 1
+    assert u1["particle"] == 20 + 1 * (20 + 8 + 20) + 8 + 1 + 3 == 80
+    assert u3["particle"] == 20 + 2 * (20 + 8 + 20) + 8 + 3 + 3 == 130
+    assert u3["tree"] == 3 and u1["split"] == 1
+    # Lorentzian g (cfg4): |x|² (2d-1) + /s² + 1 + reciprocal (div 8) + amp, then Π *= g
+    assert u3["leaf"] == 5 + 1 + 1 + 8 + 1 + 1
+    # Gaussian g (cfg2, d = 1): x² + /s² + exp 15 + amp, then Π *= g
+    assert u1["leaf"] == 1 + 1 + 15 + 1 + 1
 
 
 def test_shared_trees_credit_the_walk_once():
