@@ -222,7 +222,9 @@ rt_status rt_trace_dev(rt_handle* h, const double* d_points, int64_t n_points, d
 rt_status rt_get_stats(const rt_handle* h, rt_stats* out);
 
 /* Launch geometry override (0 = automatic): CTAs of the tree-walk kernel
- * and trees per task.  Changes only summation order. */
+ * and trees per task; in shared-tree mode (rt_eq_params.shared) the second
+ * value instead caps the trees per chunk (one phase-1 + phase-2 pass each,
+ * DESIGN.md §12).  Changes only summation order. */
 rt_status rt_set_launch(rt_handle* h, int32_t grid_ctas, int64_t trees_per_task);
 
 /* Stack-pool override (0 = automatic): at most pool_entries pending sibling

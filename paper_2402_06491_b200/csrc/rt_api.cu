@@ -471,7 +471,8 @@ static rt_status run_walk_shared(rt_handle* h, KernelFn prod, int smem, int pool
   for (int q = 0; q < nz.n_support; ++q) kmax = std::max(kmax, nz.support[q]);
   const int lmax = 1 + p.K * std::max(0, kmax - 1);           // leaves of a kept tree
   const double per_tree = static_cast<double>(lmax) * d * 8 + sizeof(rtk::TreeSum);
-  const int64_t M = std::max<int64_t>(1, std::min<int64_t>(n_trees, static_cast<int64_t>(4.0e9 / per_tree)));
+  int64_t M = std::max<int64_t>(1, std::min<int64_t>(n_trees, static_cast<int64_t>(4.0e9 / per_tree)));
+  if (h->tpt_override > 0) M = std::min(M, h->tpt_override);   // (tests: force several chunks)
   const int64_t n_chunks = (n_trees + M - 1) / M;
   // phase 2 geometry: 64 or 128 nodes (1 or 2 per thread) x tpb trees per
   // CTA; about four waves of resident CTAs per chunk (the last wave's tail

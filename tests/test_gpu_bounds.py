@@ -26,7 +26,7 @@ def test_parity_suite_under_bounds_checks():
     assert which.stdout.strip().endswith("librt_debug.so"), which.stdout + which.stderr
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
                         os.path.join(HERE, "test_gpu_parity.py"), os.path.join(HERE, "test_gpu_pdd.py"),
-                        "-k", "tree_parity or pool or extreme or geometry or pdd_downstream or edge"],
+                        "-k", "tree_parity or pool or extreme or geometry or pdd_downstream or edge or chunks"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     tail = r.stdout.strip().splitlines()[-1]

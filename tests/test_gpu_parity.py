@@ -241,6 +241,29 @@ def test_stack_pool_overflow(P, orc, name, pool):
     assert np.array_equal(s_small, ref_sums), "pool size changed the sums"
 
 
+@pytest.mark.parametrize("name,chunk", [("sh_cfg2", 377), ("sh_cfg4", 23), ("sh_ex1B", 1000)])
+def test_shared_trees_in_chunks(P, orc, name, chunk):
+    """Shared trees processed in several chunks (phase 1 + bin sort + phase 2
+    per chunk; the chunk cap forced small, ragged last chunk):
+    per-(node, tree) records equal the oracle's, bin counts are exact and the
+    sums match the oracle's and the one-chunk launch's up to summation order."""
+    eq, pts, t, N = CASES[name]
+    x = dev(pts)
+    est = P.Estimator(eq)
+    one = est.sums(x, t, N, seed=41).cpu().numpy()
+    est.set_launch(0, chunk)
+    rec, sums = est.trace(x, t, N, seed=41)
+    assert_trees_equal(rec, orc.trees(eq, pts, t, N, seed=41), eq["K"])
+    s_ref, _ = orc.sums(eq, pts, t, N, seed=41)
+    s = sums.cpu().numpy()
+    assert np.array_equal(s[:, :, 2], s_ref[:, :, 2]) and np.array_equal(s[:, :, 2], one[:, :, 2])
+    assert_nodes_close(s[:, :, 0], s_ref[:, :, 0], what="sum C")
+    assert_nodes_close(s[:, :, 1], s_ref[:, :, 1], what="sum C^2")
+    assert_nodes_close(s[:, :, 0], one[:, :, 0], what="sum C, chunked vs one chunk")
+    again = est.sums(x, t, N, seed=41).cpu().numpy()
+    assert np.array_equal(again, s), "chunked shared-tree sums not run-to-run identical"
+
+
 @pytest.mark.parametrize("name", ["cfg2", "cfg2_t2", "cfg1", "cfg3", "cfg4", "heat_d2_tanh", "d3_gauss"])
 def test_fp32_positions_variant(P, orc, name):
     """RT_PREC_FP32_POS (cfg5's FP32-position / FP64-accumulate variant): the
