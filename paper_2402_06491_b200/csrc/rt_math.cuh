@@ -238,6 +238,18 @@ RTM_HD double sqrt_nr(double a) {
   return a > 0.0 ? s : 0.0;
 }
 
+// sqrt(a) for a positive normal a (the Box–Muller radii: −2 ln v > 0 and
+// h > 0 always): sqrt_nr without the a = 0 select.
+RTM_HD double sqrt_pos(double a) {
+  double y = rsqrt_seed(a);
+  const double h = 0.5 * a;
+  const double t = h * y;
+  y = fma_d(y, fma_d(-t, y, 0.5), y);
+  double s = a * y;
+  const double r = fma_d(-s, s, a);
+  return fma_d(r, 0.5 * y, s);
+}
+
 // 1/d for normal d > 0: rcp seed and one cubic correction y(1 + e + e²).
 RTM_HD double rcp_nr(double d) {
   const double y = rcp_seed(d);

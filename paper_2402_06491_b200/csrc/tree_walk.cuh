@@ -504,11 +504,11 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     } else
     if constexpr (DIM == 1) {                   // the cosine normal only
       const double v1 = unif53(r1.x, r1.y), v2 = unif53(r1.z, r1.w);
-      const double rad = sqrt_nr(-2.0 * log_tab(v1, ltab) * h2d);
+      const double rad = sqrt_pos(-2.0 * log_tab(v1, ltab) * h2d);
       y[0] = fma(rad, cospi2(2.0 * v2), y[0]);
     } else if constexpr (DIM == 2) {
       const double v1 = unif53(r1.x, r1.y), v2 = unif53(r1.z, r1.w);
-      const double rad = sqrt_nr(-2.0 * log_tab(v1, ltab) * h2d);
+      const double rad = sqrt_pos(-2.0 * log_tab(v1, ltab) * h2d);
       double sn, cs;
       sincospi2(2.0 * v2, sn, cs);
       y[0] = fma(rad, cs, y[0]);
@@ -529,12 +529,12 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
         w4 = ((r0.x & 0xFFFu) << 20) | ((r1.x & 0xFFFu) << 8) | ((r1.z & 0xFFFu) >> 4);
         w2 = r0.w;
       }
-      const double rad = sqrt_nr(-2.0 * log_tab(v1, ltab) * h2d);
+      const double rad = sqrt_pos(-2.0 * log_tab(v1, ltab) * h2d);
       double sn, cs;
       sincos2pi_u32(w2, sn, cs);
       y[0] = fma(rad, cs, y[0]);
       y[1] = fma(rad, sn, y[1]);
-      const double rad2 = sqrt_nr(-2.0 * log_tab(v3, ltab) * h2d);
+      const double rad2 = sqrt_pos(-2.0 * log_tab(v3, ltab) * h2d);
       y[2] = fma(rad2, cos2pi_u32(w4), y[2]);
     }
     // categorical offspring choice from the integer thresholds (R9)

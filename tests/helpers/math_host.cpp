@@ -9,6 +9,7 @@ void m_sincospi2(const double* a, long n, double* s, double* c) { for (long i = 
 void m_sincos2pi_u32(const unsigned* w, long n, double* s, double* c) { for (long i = 0; i < n; ++i) sincos2pi_u32(w[i], s[i], c[i]); }
 void m_cos2pi_u32(const unsigned* w, long n, double* c) { for (long i = 0; i < n; ++i) c[i] = cos2pi_u32(w[i]); }
 void m_sqrt(const double* x, long n, double* y) { for (long i = 0; i < n; ++i) y[i] = sqrt_nr(x[i]); }
+void m_sqrt_pos(const double* x, long n, double* y) { for (long i = 0; i < n; ++i) y[i] = sqrt_pos(x[i]); }
 void m_rcp(const double* x, long n, double* y) { for (long i = 0; i < n; ++i) y[i] = rcp_nr(x[i]); }
 void m_exp(const double* x, long n, double* y) { for (long i = 0; i < n; ++i) y[i] = exp_neg(x[i]); }
 }

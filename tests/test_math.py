@@ -127,6 +127,17 @@ def test_u32_angle_reductions_bitwise(m):
     assert np.array_equal(c2.view(np.uint64), c1.view(np.uint64))
 
 
+def test_sqrt_pos_equals_sqrt_nr_on_positive_normals(m):
+    """sqrt_pos (the kernel's Box–Muller radii, argument always > 0) is
+    sqrt_nr without the zero select: bitwise equal on positive normals."""
+    x = np.exp(np.random.default_rng(13).uniform(-700, 700, 300_000))
+    a = _call(m, "m_sqrt", x)
+    m.m_sqrt_pos.argtypes = [C.c_void_p, C.c_long, C.c_void_p]
+    b = np.empty_like(x)
+    m.m_sqrt_pos(x.ctypes.data, x.size, b.ctypes.data)
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
 def test_sqrt_rcp(m):
     rng = np.random.default_rng(4)
     x = np.concatenate([np.exp(rng.uniform(-80, 80, 300_000)), [0.0, 1.0, 4.0, 2.0 ** -60]])
