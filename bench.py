@@ -236,13 +236,16 @@ def run_reference(args, cfg):
 METRIC = "random trees/sec and leaf-evals/sec on 1 B200; % of FP64 issue roofline"
 
 
-def _config_json(cfg, ws):
+def _config_json(cfg, ws, graphed=None):
     eq = cfg["eq"]
-    return {"workload": cfg["name"], "nodes": int(len(W.nodes(cfg))), "trees_per_node": cfg["n_trees"],
+    d = {"workload": cfg["name"], "nodes": int(len(W.nodes(cfg))), "trees_per_node": cfg["n_trees"],
             "dim": eq["dim"], "t": cfg["t"], "K": eq["K"], "pade": f"[{cfg['L']}/{cfg['M']}]",
             "b": eq["b"][: eq["degree"] + 1], "g": ["const", "tanh_step", "gauss", "lorentz"][eq["init_kind"]],
             "parallelism": f"trees sharded over {ws} GPU(s)" if ws > 1 else "1 GPU",
             "l2": "256 MiB buffer written between timed steps (inputs are KB-sized)"}
+    if graphed is not None:
+        d["steps_as"] = "CUDA graph replays (one captured graph per step)" if graphed else "eager launches"
+    return d
 
 
 def main():
@@ -254,6 +257,9 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--trees", type=int, default=0, help="override trees per node")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay each timed step as a captured CUDA graph (auto: on at N=1) so "
+                         "latency-bound configs are not timed on Python launch overhead")
     args = ap.parse_args()
     cfg = W.get(args.config)
     cfg["name"] = args.config
@@ -285,11 +291,12 @@ def main():
     off, n_rank = tree_range(rank, ws, N)
 
     def step(walk=None):
+        cur = torch.cuda.current_stream()    # (the capture stream inside a graph capture)
         if walk is not None:
-            walk[0].record(stream)
+            walk[0].record(cur)
         est.sums(x, t, n_rank, seed, tree_offset=off, out=sums)
         if walk is not None:
-            walk[1].record(stream)
+            walk[1].record(cur)
         merge_sums(sums)                     # one all-reduce of (K+2)x3 doubles per node
         c, se, us, ses = P.finalize(sums, K, N * ws)
         u, fl = P.pade(c, L, M)
@@ -305,8 +312,30 @@ def main():
     # the tree-walk call of each step (its memset, walk and task reduction;
     # the walk is > 99.9 % of it), events on the launch stream — no host sync
     # inside the timed region, so the steps are enqueued back to back
-    walk_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
+    def _tev():
+        # external: recorded inside a captured graph as a timed external event node
+        try:
+            return torch.cuda.Event(enable_timing=True, external=True)
+        except TypeError:
+            return torch.cuda.Event(enable_timing=True)
+    walk_ev = [(_tev(), _tev()) for _ in range(args.steps)]
+    # one captured graph per timed step (its own walk events), replayed in the
+    # timed loop: the same kernels with the same arguments, without the host's
+    # per-launch overhead between them (matters only for latency-bound configs)
+    graphs = None
+    if args.graph == "on" or (args.graph == "auto" and ws == 1):
+        try:
+            graphs = []
+            for s_ in range(args.steps):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    step(walk_ev[s_])
+                graphs.append(g)
+            torch.cuda.synchronize()
+        except Exception as e:  # noqa: BLE001 — timing method only; the kernels are the same
+            print(f"[bench] CUDA graph capture unavailable ({e}); timing eager steps", file=sys.stderr)
+            graphs = None
+            torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -314,7 +343,10 @@ def main():
         for s in range(args.steps):
             flush.fill_(s)                        # evict L2 between timed steps
             ev[s][0].record(stream)
-            u, ses = step(walk_ev[s])
+            if graphs is not None:
+                graphs[s].replay()
+            else:
+                u, ses = step(walk_ev[s])
             ev[s][1].record(stream)
         torch.cuda.synchronize()
         if dist is not None:
@@ -400,7 +432,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "trees/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": _config_json(cfg, ws),
+        "config": _config_json(cfg, ws, graphs is not None),
         "leaf_evals_per_s": leaves_all / (tot_ms / 1e3),
         "particles_per_s": st_one["particles"] * ws * args.steps / (tot_ms / 1e3),
         "pruned_fraction": st_one["pruned"] / max(1, st_one["trees"]),
