@@ -348,6 +348,12 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 
   // Transpose the pending records into the bin sums: lane b owns bin b and
   // accumulates, in ring order, ΣC, ΣC², count of the records of bin b.
+  // With at most 16 bins (K <= 14) the two half-warps split the records:
+  // lanes b and 16 + b both own bin b, the low half taking records 4i, 4i+1
+  // and the high half 4i+2, 4i+3 (one 8-byte code load and one 16-byte value
+  // load per half and step); the two partial sums are added at task close in
+  // a fixed order, so results stay a function of the task alone.
+  const bool halves = P.nb <= 16;                 // warp-uniform
   auto flush = [&]() {
     // pad the ring to a multiple of 4 with a code no lane owns, then read 4
     // records per step with 16-byte loads (codes int4, values 2 x double2)
@@ -356,14 +362,25 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     __syncwarp();
     double s1 = bsum[lane], s2 = bsum[32 + lane];
     int nn = 0;
-    for (int r = 0; r < padded; r += 4) {
-      const int4 cd = *reinterpret_cast<const int4*>(ringCode + r);
-      const double2 ca = *reinterpret_cast<const double2*>(ringC + r);
-      const double2 cb = *reinterpret_cast<const double2*>(ringC + r + 2);
-      bin_add(cd.x, lane, ca.x, s1, s2, nn);
-      bin_add(cd.y, lane, ca.y, s1, s2, nn);
-      bin_add(cd.z, lane, cb.x, s1, s2, nn);
-      bin_add(cd.w, lane, cb.y, s1, s2, nn);
+    if (halves) {
+      const int b = lane & 15;
+      const int hoff = (lane >> 4) * 2;
+      for (int r = 0; r < padded; r += 4) {
+        const int2 cd = *reinterpret_cast<const int2*>(ringCode + r + hoff);
+        const double2 ca = *reinterpret_cast<const double2*>(ringC + r + hoff);
+        bin_add(cd.x, b, ca.x, s1, s2, nn);
+        bin_add(cd.y, b, ca.y, s1, s2, nn);
+      }
+    } else {
+      for (int r = 0; r < padded; r += 4) {
+        const int4 cd = *reinterpret_cast<const int4*>(ringCode + r);
+        const double2 ca = *reinterpret_cast<const double2*>(ringC + r);
+        const double2 cb = *reinterpret_cast<const double2*>(ringC + r + 2);
+        bin_add(cd.x, lane, ca.x, s1, s2, nn);
+        bin_add(cd.y, lane, ca.y, s1, s2, nn);
+        bin_add(cd.z, lane, cb.x, s1, s2, nn);
+        bin_add(cd.w, lane, cb.y, s1, s2, nn);
+      }
     }
     ring_cnt = 0;
     bsum[lane] = s1;
@@ -382,10 +399,17 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       if (lane < P.nb) {
         RT_CHECK(task >= 0 && task < P.n_tasks);
         double* o = P.partials + (static_cast<int64_t>(task) * P.nb + lane) * 3;
-        o[0] = bsum[lane];
-        o[1] = bsum[32 + lane];
-        o[2] = static_cast<double>(bcnt[lane]);
+        if (halves) {                              // low-half records first, then high-half
+          o[0] = bsum[lane] + bsum[16 + lane];
+          o[1] = bsum[32 + lane] + bsum[48 + lane];
+          o[2] = static_cast<double>(bcnt[lane] + bcnt[16 + lane]);
+        } else {
+          o[0] = bsum[lane];
+          o[1] = bsum[32 + lane];
+          o[2] = static_cast<double>(bcnt[lane]);
+        }
       }
+      __syncwarp();
       bsum[lane] = 0.0;
       bsum[32 + lane] = 0.0;
       bcnt[lane] = 0;
