@@ -88,7 +88,7 @@ struct rt_handle {
   cudaStream_t last_stream = nullptr;
   bool have_timing = false;
   double host_total_ms = -1.0;
-  DevBuf partials, gpool, gaux, wtime, sh_tsum, sh_leaves, sh_sorted, sh_boff, pdd_pts, pdd_nodal, pdd_bc, pdd_field, pdd_c, pdd_u, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
+  DevBuf partials, gpool, gaux, lacc, wtime, sh_tsum, sh_leaves, sh_sorted, sh_boff, pdd_pts, pdd_nodal, pdd_bc, pdd_field, pdd_c, pdd_u, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
   int32_t grid_override = 0;
   int64_t tpt_override = 0;
   int32_t pool_override = 0;
@@ -224,7 +224,7 @@ extern "C" rt_status rt_destroy(rt_handle* h) {
   if (!h) return RT_OK;
   if (h->own_stream) cudaStreamSynchronize(h->own_stream);
   if (h->last_stream) cudaStreamSynchronize(h->last_stream);
-  for (DevBuf* b : {&h->partials, &h->gpool, &h->gaux, &h->wtime, &h->sh_tsum, &h->sh_leaves, &h->sh_sorted, &h->sh_boff, &h->pdd_pts, &h->pdd_nodal,
+  for (DevBuf* b : {&h->partials, &h->gpool, &h->gaux, &h->lacc, &h->wtime, &h->sh_tsum, &h->sh_leaves, &h->sh_sorted, &h->sh_boff, &h->pdd_pts, &h->pdd_nodal,
                     &h->pdd_bc, &h->pdd_field, &h->pdd_c, &h->pdd_u, &h->sums, &h->stats, &h->h_points, &h->h_coeffs,
                     &h->h_stderr, &h->h_aux, &h->h_flags})
     b->release();
@@ -602,6 +602,8 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   const size_t nwarps = static_cast<size_t>(L.grid) * rtk::kWarpsPerCta;
   RT_CUDA(h->gpool.ensure(nwarps * gcap * nf * sizeof(double)));
   RT_CUDA(h->gaux.ensure(nwarps * 2 * gcap * sizeof(int32_t)));
+  // lane-private order-bin sums (RED targets): [warps][nb][ΣC, ΣC², n][32]
+  RT_CUDA(h->lacc.ensure(nwarps * nb * 96 * sizeof(double)));
   if (h->pool_override > 0) pool_cap = std::min(pool_cap, static_cast<int>(h->pool_override));
 
   WalkParams P;
@@ -617,6 +619,7 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   P.pool_cap = pool_cap;
   P.gpool = static_cast<double*>(h->gpool.p);
   P.gaux = static_cast<int32_t*>(h->gaux.p);
+  P.lacc = static_cast<double*>(h->lacc.p);
   P.gcap = gcap;
   P.recs = d_recs;
   P.rec_shift = rec_shift;

@@ -23,15 +23,17 @@
 // A group stores the split position y, remaining horizon τ_c and a packed
 // (next child label | remaining count << 56).
 //
-// Order binning: a finished tree appends
-// (bin, C) to a 64-entry per-warp ring in shared memory; when 32 records are
-// pending the warp "transposes" them: lane b owns order bin b and
-// accumulates, in ring order, the records whose bin is b (ΣC, ΣC², count).
-// When all trees of a task are recorded, lane b writes the task's bin b to
-// partials[task][b] (atomic-free); a second kernel sums each node's tasks in
-// task order.  Each task runs from a clean start (all lanes begin it
-// together), so its partials depend on the task alone: results are bitwise
-// reproducible for a fixed task size, whatever the grid or warp timing.
+// Order binning: a lane whose tree finishes adds
+// C, C² and 1 to ITS OWN accumulators of the tree's order bin, lane-private
+// words in global memory ([warp][bin][ΣC, ΣC², n][lane], L2-resident) updated
+// with fire-and-forget atomic adds (RED): one writer per word and program
+// order, so the sums are deterministic.  When all trees of a task are
+// recorded, every lane reads back and clears its words (L2 loads) and the
+// warp adds the 32 lanes' sums of each bin in a fixed butterfly order into
+// partials[task][bin]; a second kernel sums each node's tasks in task order.
+// Each task runs from a clean start (all lanes begin it together), so its
+// partials depend on the task alone: results are bitwise reproducible for a
+// fixed task size, whatever the grid or warp timing.
 #pragma once
 #include <cstdint>
 #include <cstdio>
@@ -60,7 +62,6 @@ namespace rtk {
 
 constexpr int kWarpsPerCta = 4;
 constexpr int kThreads = 32 * kWarpsPerCta;
-constexpr int kRing = 64;   // >= 31 pending + 32 new records, padded to 4
 constexpr uint64_t kLabelMask = (1ull << 56) - 1;
 
 // Stack-pool entries per warp in shared memory (<= 255: 8-bit free list) and
@@ -69,9 +70,9 @@ constexpr uint64_t kLabelMask = (1ull << 56) - 1;
 // record-emitting trace variant gets one CTA less so it never spills; it is
 // launched on the production kernel's grid, so both give identical sums.
 template <int DIM> struct PoolCap;
-template <> struct PoolCap<1> { static constexpr int v = 144; };
-template <> struct PoolCap<2> { static constexpr int v = 136; };
-template <> struct PoolCap<3> { static constexpr int v = 112; };
+template <> struct PoolCap<1> { static constexpr int v = 192; };
+template <> struct PoolCap<2> { static constexpr int v = 176; };
+template <> struct PoolCap<3> { static constexpr int v = 144; };
 template <int DIM, bool REC> struct MinCtas {
   static constexpr int v = 8 - (REC ? 1 : 0);
 };
@@ -102,6 +103,7 @@ struct WalkParams {
   int32_t pool_cap;                   // shared-memory pool entries used (<= PoolCap)
   double* partials;     // [n_tasks][nb][3]
   double* gpool;        // [warps][gcap][DIM+2]  overflow stack entries
+  double* lacc;         // [warps][nb][3][32] lane-private order-bin sums (ΣC, ΣC², count)
   int32_t* gaux;        // [warps][2][gcap]      overflow prev links, free list
   int32_t gcap;         // overflow entries per warp (32 (K+1): every stack bound)
   TreeRec* recs;
@@ -140,6 +142,7 @@ struct WarpState {
   int gtop, gfree;          // overflow area: bump pointer, free-list size
   double* gpool;            // the warp's overflow area (read in the slow paths only,
   int* gprev;               //   so the compiler does not keep or rematerialise them)
+  double* lacc;             // the warp's lane accumulators
 };
 
 // The initial data g: constant, tanh step, Gaussian,
@@ -185,13 +188,11 @@ __device__ __forceinline__ float g_eval_f(const float (&x)[DIM], const WalkParam
   }
 }
 
-// per-warp shared memory: pool fields [DIM+2][cap] doubles, ring (C, code)
-// [kRing], bin sums [ΣC, ΣC²][32] + counts [32], state, prev [cap] int16,
-// free list [cap] u8
+// per-warp shared memory: pool fields [DIM+2][cap] doubles, state, prev [cap]
+// int16, free list [cap] u8
 template <int DIM>
 __host__ __device__ constexpr int warp_smem_bytes() {
-  return PoolCap<DIM>::v * ((DIM + 2) * 8 + 2 + 1) + kRing * 12 + 2 * 32 * 8 + 32 * 4 +
-         static_cast<int>(sizeof(WarpState));
+  return PoolCap<DIM>::v * ((DIM + 2) * 8 + 2 + 1) + static_cast<int>(sizeof(WarpState));
 }
 
 template <int DIM>
@@ -211,16 +212,10 @@ __device__ __forceinline__ void inc_if(bool c, int& n) {
       : "+r"(n) : "r"(static_cast<int>(c)));
 }
 
-// Ring transposition step: lane b adds record (code, C) to its bin sums iff
-// code == b, as x = (code == b ? C : 0), s1 += x, s2 += x² — one select, no
-// branch (bitwise the conditional sums: s1 is never -0, and 0² leaves s2; the
-// padding records' C is never read into an operand that survives)
-__device__ __forceinline__ void bin_add(int code, int lane, double c, double& s1, double& s2, int& nn) {
-  const bool own = code == lane;
-  const double x = own ? c : 0.0;
-  inc_if(own, nn);
-  s1 += x;
-  s2 = fma(x, x, s2);
+// Fire-and-forget FP64 add to a global word (RED; the generic atomicAdd on a
+// pointer read from shared memory would also test for the shared window)
+__device__ __forceinline__ void red_add(double* p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
 // F32 = the FP32-position / FP64-accumulate variant (cfg5, BASELINE.json
@@ -251,12 +246,8 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   const int wstride = warp_stride<DIM>();
   unsigned char* const wbase = smem_raw + 128 * 16 + wib * wstride;
   double* const pool = reinterpret_cast<double*>(wbase);                   // [NF][CAP]
-  double* const ringC = pool + NF * CAP;                                    // [kRing]
-  double* const bsum = ringC + kRing;                                       // [ΣC, ΣC²][32]
-  int* const bcnt = reinterpret_cast<int*>(bsum + 2 * 32);                  // [32]
-  WarpState* const ws = reinterpret_cast<WarpState*>(bcnt + 32);
-  int* const ringCode = reinterpret_cast<int*>(ws + 1);                     // [kRing]
-  int16_t* const prevS = reinterpret_cast<int16_t*>(ringCode + kRing);      // [CAP]
+  WarpState* const ws = reinterpret_cast<WarpState*>(pool + NF * CAP);
+  int16_t* const prevS = reinterpret_cast<int16_t*>(ws + 1);               // [CAP]
   uint8_t* const freeS = reinterpret_cast<uint8_t*>(prevS + CAP);           // [CAP]
   double* const wtab = reinterpret_cast<double*>(smem_raw + 128 * 16 +
       kWarpsPerCta * wstride);                                           // [9] weights
@@ -268,17 +259,21 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   }
   const int cap = P.pool_cap;
   for (int q = lane; q < cap; q += 32) freeS[q] = static_cast<uint8_t>(q);
-  bsum[lane] = 0.0;
-  bsum[32 + lane] = 0.0;
-  bcnt[lane] = 0;
 
   const int gwarp = blockIdx.x * kWarpsPerCta + wib;
   if (P.wtime != nullptr && lane == 0) P.wtime[4 * gwarp] = global_ns();
   if (lane == 0) {
     ws->gpool = P.gpool + static_cast<int64_t>(gwarp) * P.gcap * NF;
     ws->gprev = P.gaux + static_cast<int64_t>(gwarp) * 2 * P.gcap;
+    ws->lacc = SH ? nullptr : P.lacc + static_cast<int64_t>(gwarp) * P.nb * 96;
   }
   __syncwarp();
+  // lane-private order-bin accumulators in global memory: [bin][ΣC, ΣC², n][lane]
+  auto lacc = [&]() -> double* { return *static_cast<double* volatile*>(&ws->lacc) + lane; };
+  if constexpr (!SH) {
+    double* a = lacc();
+    for (int b = 0; b < P.nb; ++b) { a[b * 96] = 0.0; a[b * 96 + 32] = 0.0; a[b * 96 + 64] = 0.0; }
+  }
   // overflow-area bases, re-read from shared memory where used (volatile: no
   // hoisting into the fast path)
   auto gpool = [&]() -> double* { return *static_cast<double* volatile*>(&ws->gpool); };
@@ -320,7 +315,6 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     }
     __syncwarp();
   };
-  int ring_cnt = 0;    // pending records (always flushed completely)
   int nfree = cap;     // free shared-memory pool entries
   int n_glob = 0;      // overflow entries in use (warp-uniform)
 
@@ -348,71 +342,31 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 
   // Transpose the pending records into the bin sums: lane b owns bin b and
   // accumulates, in ring order, ΣC, ΣC², count of the records of bin b.
-  // With at most 16 bins (K <= 14) the two half-warps split the records:
-  // lanes b and 16 + b both own bin b, the low half taking records 4i, 4i+1
-  // and the high half 4i+2, 4i+3 (one 8-byte code load and one 16-byte value
-  // load per half and step); the two partial sums are added at task close in
-  // a fixed order, so results stay a function of the task alone.
-  const bool halves = P.nb <= 16;                 // warp-uniform
-  auto flush = [&]() {
-    // pad the ring to a multiple of 4 with a code no lane owns, then read 4
-    // records per step with 16-byte loads (codes int4, values 2 x double2)
-    const int padded = (ring_cnt + 3) & ~3;
-    if (ring_cnt + lane < padded) ringCode[ring_cnt + lane] = -1;
-    __syncwarp();
-    double s1 = bsum[lane], s2 = bsum[32 + lane];
-    int nn = 0;
-    if (halves) {
-      const int b = lane & 15;
-      const int hoff = (lane >> 4) * 2;
-      for (int r = 0; r < padded; r += 4) {
-        const int2 cd = *reinterpret_cast<const int2*>(ringCode + r + hoff);
-        const double2 ca = *reinterpret_cast<const double2*>(ringC + r + hoff);
-        bin_add(cd.x, b, ca.x, s1, s2, nn);
-        bin_add(cd.y, b, ca.y, s1, s2, nn);
-      }
-    } else {
-      for (int r = 0; r < padded; r += 4) {
-        const int4 cd = *reinterpret_cast<const int4*>(ringCode + r);
-        const double2 ca = *reinterpret_cast<const double2*>(ringC + r);
-        const double2 cb = *reinterpret_cast<const double2*>(ringC + r + 2);
-        bin_add(cd.x, lane, ca.x, s1, s2, nn);
-        bin_add(cd.y, lane, ca.y, s1, s2, nn);
-        bin_add(cd.z, lane, cb.x, s1, s2, nn);
-        bin_add(cd.w, lane, cb.y, s1, s2, nn);
-      }
-    }
-    ring_cnt = 0;
-    bsum[lane] = s1;
-    bsum[32 + lane] = s2;
-    bcnt[lane] += nn;
-    __syncwarp();
-  };
-
   // All trees of the task are recorded: write its partials (lane b = bin b),
   // fold the event counters, fetch the next task and start its first trees.
   auto close_and_next = [&]() {
     if constexpr (SH) {
       // phase 1 writes tree summaries only (phase 2 accumulates per node)
     } else {
-      flush();
-      if (lane < P.nb) {
-        RT_CHECK(task >= 0 && task < P.n_tasks);
-        double* o = P.partials + (static_cast<int64_t>(task) * P.nb + lane) * 3;
-        if (halves) {                              // low-half records first, then high-half
-          o[0] = bsum[lane] + bsum[16 + lane];
-          o[1] = bsum[32 + lane] + bsum[48 + lane];
-          o[2] = static_cast<double>(bcnt[lane] + bcnt[16 + lane]);
-        } else {
-          o[0] = bsum[lane];
-          o[1] = bsum[32 + lane];
-          o[2] = static_cast<double>(bcnt[lane]);
+      // each lane reads back (L2: its own atomics) and clears its sums, the
+      // warp adds the 32 lanes' in a fixed butterfly order, lane 0 writes
+      RT_CHECK(task >= 0 && task < P.n_tasks);
+      __threadfence();                             // this lane's REDs are performed before its read-back
+      double* a = lacc();
+      for (int b = 0; b < P.nb; ++b) {
+        double v1 = __ldcg(a + b * 96), v2 = __ldcg(a + b * 96 + 32), v3 = __ldcg(a + b * 96 + 64);
+        a[b * 96] = 0.0; a[b * 96 + 32] = 0.0; a[b * 96 + 64] = 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+          v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+          v3 += __shfl_xor_sync(0xffffffffu, v3, o);
+        }
+        if (lane == 0) {
+          double* o = P.partials + (static_cast<int64_t>(task) * P.nb + b) * 3;
+          o[0] = v1; o[1] = v2; o[2] = v3;
         }
       }
-      __syncwarp();
-      bsum[lane] = 0.0;
-      bsum[32 + lane] = 0.0;
-      bcnt[lane] = 0;
     }
     // (shared trees: every node sees each walked particle and leaf)
     const unsigned long long scale = SH ? static_cast<unsigned long long>(P.n_points) : 1ull;
@@ -767,12 +721,14 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
           P.tsum[tj - static_cast<uint32_t>(P.tree_offset)] = ts;
         }
       } else {
-        if (done) {
-          RT_CHECK(ring_cnt + rank < kRing);
-          ringCode[ring_cnt + rank] = ne;             // = K+1 (the pruned bin) iff pruned
-          ringC[ring_cnt + rank] = pruned ? 0.0 : Pi;
+        const double cv = pruned ? 0.0 : Pi;          // (a pruned tree adds 0 to the sums)
+        if (done) {                                 // bin ne (= K+1, the pruned bin, iff pruned)
+          RT_CHECK(ne >= 0 && ne < P.nb);
+          double* a = lacc() + ne * 96;
+          red_add(a, cv);
+          red_add(a + 32, cv * cv);
+          red_add(a + 64, 1.0);
         }
-        ring_cnt += nfin;
       }
       left -= nfin;
       const uint32_t avail = iss_end - iss_next;
@@ -789,10 +745,8 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
         iss_next += avail;
         if (left == 0) close_and_next();                   // every tree recorded
       }
-      if (ring_cnt >= 32) flush();
     }
   }
-  if (ring_cnt > 0) flush();
   if (P.wtime != nullptr && lane == 0) {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
