@@ -554,7 +554,8 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const bool branch = split && !pruned && !kill;
     // g at a leaf; h^(α) = c'_α at a split; 0 if killed
     const double gl = SH ? 1.0 : gv;            // SH: g is applied per node below
-    const double fac = leaf ? (SB ? gl * P.inv_q : gl) : (kill ? 0.0 : wk);
+    // (a pruned or killed tree's product becomes 0: it adds nothing to the sums)
+    const double fac = leaf ? (SB ? gl * P.inv_q : gl) : ((kill || pruned) ? 0.0 : wk);
     if (active) Pi *= fac;
     inc_if(active, c_part);
     inc_if(active && leaf, c_leaf);
@@ -721,12 +722,11 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
           P.tsum[tj - static_cast<uint32_t>(P.tree_offset)] = ts;
         }
       } else {
-        const double cv = pruned ? 0.0 : Pi;          // (a pruned tree adds 0 to the sums)
-        if (done) {                                 // bin ne (= K+1, the pruned bin, iff pruned)
+        if (done) {                                 // bin ne (= K+1, the pruned bin, iff pruned; Π = 0 then)
           RT_CHECK(ne >= 0 && ne < P.nb);
           double* a = lacc() + ne * 96;
-          red_add(a, cv);
-          red_add(a + 32, cv * cv);
+          red_add(a, Pi);
+          red_add(a + 32, Pi * Pi);
           red_add(a + 64, 1.0);
         }
       }
