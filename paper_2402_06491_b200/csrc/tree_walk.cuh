@@ -556,7 +556,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const double gl = SH ? 1.0 : gv;            // SH: g is applied per node below
     // (a pruned or killed tree's product becomes 0: it adds nothing to the sums)
     const double fac = leaf ? (SB ? gl * P.inv_q : gl) : ((kill || pruned) ? 0.0 : wk);
-    if (active) Pi *= fac;
+    Pi *= fac;                                   // (an idle lane's product is never recorded)
     inc_if(active, c_part);
     inc_if(active && leaf, c_leaf);
     if constexpr (REC || SH) {
