@@ -548,14 +548,15 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 
     // ---------------- tree logic: predicated straight-line code ---------------
     const bool split = active && !leaf;
-    inc_if(split, ne);                           // splitting events
+    inc_if(!leaf, ne);                           // splitting events (an idle lane's ne is unused)
     const bool pruned = split && ne > P.K;       // prune
-    const bool kill = split && !pruned && P.n_support == 0;   // purely linear f
-    const bool branch = split && !pruned && !kill;
-    // g at a leaf; h^(α) = c'_α at a split; 0 if killed
+    // a pruned tree (ne = K+1, the pruned bin) and a killed one (purely linear
+    // f: no offspring, bin ne) both end here with a zero product
+    const bool dead = split && (ne > P.K || P.n_support == 0);
+    const bool branch = split && !dead;
+    // g at a leaf; h^(α) = c'_α at a split
     const double gl = SH ? 1.0 : gv;            // SH: g is applied per node below
-    // (a pruned or killed tree's product becomes 0: it adds nothing to the sums)
-    const double fac = leaf ? (SB ? gl * P.inv_q : gl) : ((kill || pruned) ? 0.0 : wk);
+    const double fac = leaf ? (SB ? gl * P.inv_q : gl) : (dead ? 0.0 : wk);
     Pi *= fac;                                   // (an idle lane's product is never recorded)
     inc_if(active, c_part);
     inc_if(active && leaf, c_leaf);
@@ -566,7 +567,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const bool push = branch && k > 1;           // k-1 younger siblings wait
     const bool pop = (active && leaf) || (branch && k == 0);
     const bool has = pop && top >= 0;            // resume the top group's next child
-    const bool done = pruned || kill || (pop && top < 0);
+    const bool done = dead || (pop && top < 0);
     // child 0 continues from the split point y with horizon τ_c (popping
     // lanes overwrite y, τ, label below; finished lanes are re-initialised)
     tau = tc;
