@@ -426,7 +426,9 @@ static void fill_params(const rt_handle* h, WalkParams& P, double t, uint64_t se
   P.inv_scale = 1.0 / p.init_scale;
   P.inv_scale2 = 1.0 / (p.init_scale * p.init_scale);
   P.t = t;
-  for (int q = 0; q < 9; ++q) P.thr[q] = 0xffffffffu;
+  // (no support — a purely linear f: every split draws entry 0, whose zero
+  // weight makes the killed tree's product 0)
+  for (int q = 0; q < 9; ++q) { P.thr[q] = 0xffffffffu; P.w[q] = 0.0; P.kval[q] = 0; }
   for (int q = 0; q < nz.n_support; ++q) {
     P.w[q] = nz.w[q];
     P.thr[q] = static_cast<uint32_t>(nz.thresh[q] - 1);

@@ -364,7 +364,8 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
         }
         if (lane == 0) {
           double* o = P.partials + (static_cast<int64_t>(task) * P.nb + b) * 3;
-          o[0] = v1; o[1] = v2; o[2] = v3;
+          const bool prb = b == P.K + 1;           // pruned bin: count only
+          o[0] = prb ? 0.0 : v1; o[1] = prb ? 0.0 : v2; o[2] = v3;
         }
       }
     }
@@ -556,7 +557,10 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const bool branch = split && !dead;
     // g at a leaf; h^(α) = c'_α at a split
     const double gl = SH ? 1.0 : gv;            // SH: g is applied per node below
-    const double fac = leaf ? (SB ? gl * P.inv_q : gl) : (dead ? 0.0 : wk);
+    // (a killed tree's wk is 0 — entry 0 of an empty support; a pruned tree
+    // keeps a nonzero product, routed to the pruned bin whose sums are
+    // discarded at task close)
+    const double fac = leaf ? (SB ? gl * P.inv_q : gl) : wk;
     Pi *= fac;                                   // (an idle lane's product is never recorded)
     inc_if(active, c_part);
     inc_if(active && leaf, c_leaf);
@@ -723,7 +727,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
           P.tsum[tj - static_cast<uint32_t>(P.tree_offset)] = ts;
         }
       } else {
-        if (done) {                                 // bin ne (= K+1, the pruned bin, iff pruned; Π = 0 then)
+        if (done) {                                 // bin ne (= K+1, the pruned bin, iff pruned)
           RT_CHECK(ne >= 0 && ne < P.nb);
           double* a = lacc() + ne * 96;
           red_add(a, Pi);
