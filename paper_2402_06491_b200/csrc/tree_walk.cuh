@@ -518,13 +518,19 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     }
     // categorical offspring choice from the integer thresholds (R9)
     // (thresholds past the support are 0xffffffff, so the sum needs no bound)
+    // (the last support entry's threshold is 2^32 - 1: with n entries only
+    // n - 1 compares can fire — two for the configs' three-term f)
     const uint32_t c32 = r0.z;
     int s = 0;
+    inc_if(c32 > P.thr[0], s);
+    inc_if(c32 > P.thr[1], s);
+    if (P.n_support > 3) {                      // warp-uniform
+      inc_if(c32 > P.thr[2], s);
+      inc_if(c32 > P.thr[3], s);
+      if (P.n_support > 5) {                    // warp-uniform, rare
 #pragma unroll
-    for (int q = 0; q < 4; ++q) inc_if(c32 > P.thr[q], s);
-    if (P.n_support > 5) {                      // warp-uniform, rare
-#pragma unroll
-      for (int q = 4; q < 8; ++q) inc_if(c32 > P.thr[q], s);
+        for (int q = 4; q < 8; ++q) inc_if(c32 > P.thr[q], s);
+      }
     }
     double gv;                                  // g at the leaf
     if constexpr (F32) gv = static_cast<double>(g_eval_f<DIM, GK>(y, P));
