@@ -237,14 +237,21 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int NF = DIM + 2;
   constexpr int CAP = PoolCap<DIM>::v;
-  const int lane = threadIdx.x & 31;
+  // lane, its lower-lanes mask and the warp's shared-memory offset are read
+  // through opaque moves, so the compiler keeps them in registers instead of
+  // rematerialising them from threadIdx every iteration
+  int lane;
+  unsigned lt_mask;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane));
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(lt_mask));
   const int wib = threadIdx.x >> 5;
-  const unsigned lt_mask = (1u << lane) - 1u;
 
   // ---- shared memory carve-up -------------------------------------------
   LogEntry* const ltab = reinterpret_cast<LogEntry*>(smem_raw);
   const int wstride = warp_stride<DIM>();
-  unsigned char* const wbase = smem_raw + 128 * 16 + wib * wstride;
+  unsigned woff;
+  asm volatile("mov.u32 %0, %1;" : "=r"(woff) : "r"(128 * 16 + wib * wstride));
+  unsigned char* const wbase = smem_raw + woff;
   double* const pool = reinterpret_cast<double*>(wbase);                   // [NF][CAP]
   WarpState* const ws = reinterpret_cast<WarpState*>(pool + NF * CAP);
   int16_t* const prevS = reinterpret_cast<int16_t*>(ws + 1);               // [CAP]
