@@ -22,7 +22,10 @@
  *     same thread).  Output buffers are unspecified after a failure.
  *   - The caller owns every input and output buffer.  rt_create copies the
  *     parameters; the handle owns its device scratch (grown lazily, freed by
- *     rt_destroy).  A handle must not be used from two threads at once.
+ *     rt_destroy).  A handle must not be used from two threads at once, and
+ *     its "_dev" calls share that scratch (task partials, lane-private bin
+ *     sums, overflow stacks): calls on different streams must be ordered by
+ *     the caller — use one handle per concurrently running stream.
  *   - "host" pointers are ordinary CPU memory; such calls are synchronous.
  *     "_dev" entry points take device pointers and a cudaStream_t (as void*;
  *     NULL = legacy default stream), are stream-ordered and do not
