@@ -465,6 +465,32 @@ def test_full_cfg4_sampled_and_closed_form(P, orc):
     assert np.array_equal(s, s2)
 
 
+def test_full_cfg3_sampled_and_closed_form(P, orc):
+    """cfg3 at full size (256 nodes x 1e6 trees, d = 2, bench launch): every
+    2^12-th tree of every node equals the oracle's; every node counts exactly
+    N trees; the order-0 coefficient matches its closed form
+    e^{-t} A (1 + 2s^2)^{-1} exp(-|x|^2 / (1 + 2s^2)), s^2 = 2Dt (the heat
+    kernel applied to the Gaussian data) within 4.42 s.e."""
+    cfg = W.get("cfg3")
+    eq, N, t = cfg["eq"], cfg["n_trees"], cfg["t"]
+    pts = W.nodes(cfg)
+    est = P.Estimator(eq)
+    rec, sums = est.trace(dev(pts), t, N, seed=cfg["seed"], rec_shift=12)
+    js = np.arange(0, N, 1 << 12)
+    assert_trees_equal(rec, orc.trees_at(eq, pts, t, js, seed=cfg["seed"]), eq["K"])
+    s = sums.cpu().numpy()
+    assert np.all(s[:, :, 2].sum(1) == N)
+    c, se, us, ses = P.finalize(sums, eq["K"], N)
+    c0 = c[:, 0].cpu().numpy(); se0 = se[:, 0].cpu().numpy()
+    s2 = 2.0 * eq["D"] * t
+    a = 1.0 + 2.0 * s2 / eq["init_scale"] ** 2
+    r2 = (np.asarray(pts) ** 2).sum(1)
+    ex = np.exp(-t) * eq["init_amp"] / a * np.exp(-r2 / (a * eq["init_scale"] ** 2))
+    z = (c0 - ex) / se0
+    assert np.max(np.abs(z)) < 4.42, np.max(np.abs(z))
+    assert np.array_equal(s, est.sums(dev(pts), t, N, seed=cfg["seed"]).cpu().numpy())
+
+
 def test_full_cfg2_closed_form_and_fd(P):
     """cfg2 at full size: c_0 = e^{-t} heat(x) within 4 s.e. at all 64 nodes;
     Padé [5/5] within 4 s.e. (+ FD error) of the FD solution at three nodes."""
