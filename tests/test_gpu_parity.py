@@ -491,6 +491,21 @@ def test_full_cfg3_sampled_and_closed_form(P, orc):
     assert np.array_equal(s, est.sums(dev(pts), t, N, seed=cfg["seed"]).cpu().numpy())
 
 
+def test_full_cfg4_shared_trees_sampled(P, orc):
+    """Shared trees (f4) at cfg4's full size (1024 nodes x 1e7 trees, 8
+    chunks): every 2^16-th tree of every node equals the oracle's shared-tree
+    record, and every node counts exactly N trees."""
+    cfg = W.get("cfg4")
+    eq, N, t = dict(cfg["eq"], shared=1), cfg["n_trees"], cfg["t"]
+    pts = W.nodes(cfg)
+    est = P.Estimator(eq)
+    rec, sums = est.trace(dev(pts), t, N, seed=cfg["seed"], rec_shift=16)
+    js = np.arange(0, N, 1 << 16)
+    assert_trees_equal(rec, orc.trees_at(eq, pts, t, js, seed=cfg["seed"]), eq["K"])
+    s = sums.cpu().numpy()
+    assert np.all(s[:, :, 2].sum(1) == N)
+
+
 def test_full_cfg2_closed_form_and_fd(P):
     """cfg2 at full size: c_0 = e^{-t} heat(x) within 4 s.e. at all 64 nodes;
     Padé [5/5] within 4 s.e. (+ FD error) of the FD solution at three nodes."""
