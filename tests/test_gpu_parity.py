@@ -506,6 +506,21 @@ def test_full_cfg4_shared_trees_sampled(P, orc):
     assert np.all(s[:, :, 2].sum(1) == N)
 
 
+@pytest.mark.parametrize("name", ["ex3B", "ex5A", "ex5B"])
+def test_full_examples_sampled(P, orc, name):
+    """The f2/f3 Examples at their bench size (Strategy A's shift, Strategy B;
+    d = 1, 2; 64 or 256 nodes x 1e6 trees, bench launch): every 2^12-th tree
+    of every node equals the oracle's; every node counts exactly N trees."""
+    cfg = W.get(name)
+    eq, N, t = cfg["eq"], cfg["n_trees"], cfg["t"]
+    pts = W.nodes(cfg)
+    est = P.Estimator(eq)
+    rec, sums = est.trace(dev(pts), t, N, seed=cfg["seed"], rec_shift=12)
+    js = np.arange(0, N, 1 << 12)
+    assert_trees_equal(rec, orc.trees_at(eq, pts, t, js, seed=cfg["seed"]), eq["K"])
+    assert np.all(sums.cpu().numpy()[:, :, 2].sum(1) == N)
+
+
 def test_full_cfg2_closed_form_and_fd(P):
     """cfg2 at full size: c_0 = e^{-t} heat(x) within 4 s.e. at all 64 nodes;
     Padé [5/5] within 4 s.e. (+ FD error) of the FD solution at three nodes."""
