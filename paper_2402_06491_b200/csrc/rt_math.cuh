@@ -100,7 +100,7 @@ RTM_HD double log_tab(double x, const LogEntry* T) {
   const double z = dfrom((static_cast<uint64_t>(hi - (tmp & 0xfff00000u)) << 32) | (ix & 0xffffffffull));
   const LogEntry e = T[i];
   const double r = fma_d(z, e.invc, -1.0);
-  double p = kLogP[5];
+  double p = kLogPTop;
   p = fma_d(p, r, kLogP[4]);
   p = fma_d(p, r, kLogP[3]);
   p = fma_d(p, r, kLogP[2]);
@@ -114,14 +114,14 @@ RTM_HD double log_tab(double x, const LogEntry* T) {
 // sin(pi f), cos(pi f) for |f| <= 1/4 (near-minimax in f², fit errors < 3e-18).
 RTM_HD void sincospi_core(double f, double& s, double& c) {
   const double f2 = f * f;
-  double ps = kSinPi[6];
+  double ps = kSinPiTop;
   ps = fma_d(ps, f2, kSinPi[5]);
   ps = fma_d(ps, f2, kSinPi[4]);
   ps = fma_d(ps, f2, kSinPi[3]);
   ps = fma_d(ps, f2, kSinPi[2]);
   ps = fma_d(ps, f2, kSinPi[1]);
   ps = fma_d(ps, f2, kSinPi[0]);
-  double pc = kCosPi[7];
+  double pc = kCosPiTop;
   pc = fma_d(pc, f2, kCosPi[6]);
   pc = fma_d(pc, f2, kCosPi[5]);
   pc = fma_d(pc, f2, kCosPi[4]);
@@ -156,7 +156,7 @@ RTM_HD double cospi2(double a) {
   const double n = rint_d(a);
   const double f = a - n;
   const double f2 = f * f;
-  double p = kCosPiW[8];
+  double p = kCosPiWTop;
   p = fma_d(p, f2, kCosPiW[7]);
   p = fma_d(p, f2, kCosPiW[6]);
   p = fma_d(p, f2, kCosPiW[5]);
@@ -184,14 +184,14 @@ RTM_HD void sincos2pi_u32(uint32_t w, double& s_out, double& c_out) {
   const uint32_t q = ((w >> 29) + 1u) >> 1;
   const double d = static_cast<double>(static_cast<int32_t>(2u * w + 1u - (q << 31)));
   const double D = d * d;
-  double ps = kSinPi32[6];
+  double ps = kSinPi32Top;
   ps = fma_d(ps, D, kSinPi32[5]);
   ps = fma_d(ps, D, kSinPi32[4]);
   ps = fma_d(ps, D, kSinPi32[3]);
   ps = fma_d(ps, D, kSinPi32[2]);
   ps = fma_d(ps, D, kSinPi32[1]);
   ps = fma_d(ps, D, kSinPi32[0]);
-  double pc = kCosPi32[7];
+  double pc = kCosPi32Top;
   pc = fma_d(pc, D, kCosPi32[6]);
   pc = fma_d(pc, D, kCosPi32[5]);
   pc = fma_d(pc, D, kCosPi32[4]);
@@ -213,7 +213,7 @@ RTM_HD void sincos2pi_u32(uint32_t w, double& s_out, double& c_out) {
 RTM_HD double cos2pi_u32(uint32_t w) {
   const double d = static_cast<double>(static_cast<int32_t>(2u * w + 1u));
   const double D = d * d;
-  double p = kCosPiW32[8];
+  double p = kCosPiW32Top;
   p = fma_d(p, D, kCosPiW32[7]);
   p = fma_d(p, D, kCosPiW32[6]);
   p = fma_d(p, D, kCosPiW32[5]);
