@@ -202,48 +202,68 @@ static double particle(tree_ctx* c, const double* y, double tau, uint64_t label)
    * horizon, the children inherit τ(1 - S).                                */
   int is_leaf;
   double h, tc;
+  double e1 = 0.0, e2 = 0.0;         /* Strategy A: the radii's Exp(1) variates */
   if (strat_b) {
     is_leaf = (uint64_t)r0[3] < nz->tq;                /* ξ = 0 */
     double Sf = or_unif53(r0[0], r0[1]);               /* S ~ U(0,1) */
     h = is_leaf ? tau : tau * Sf;
     tc = tau * (1.0 - Sf);
   } else {
-    double S = -log(or_unif53(r0[0], r0[1])) * nz->inv_lambda;
+    /* DESIGN.md R29: G = -log(U_1 ... U_{m+1}) ~ Gamma(m+1) split by the
+     * spacings of m sorted uniforms into m+1 iid Exp(1) variates: e0 for the
+     * clock, e1 (e2) for the Box-Muller radii r = sqrt(2e).               */
+    double u12 = or_unif32(r0[0]) * or_unif32(r0[1]);
+    double e0;
+    if (p->dim <= 2) {
+      double v = or_unif32(r0[3]);
+      double G = -log(u12);
+      e0 = G * v;
+      e1 = G * (1.0 - v);
+    } else {
+      uint32_t lo = r1[1] < r1[2] ? r1[1] : r1[2], hi = r1[1] < r1[2] ? r1[2] : r1[1];
+      double v1 = or_unif32(lo), v2 = or_unif32(hi);
+      double G = -log(u12 * or_unif32(r1[0]));
+      e0 = G * v1;
+      e1 = G * (v2 - v1);
+      e2 = G * (1.0 - v2);
+    }
+    double S = e0 * nz->inv_lambda;                    /* S ~ λ e^{-λS} */
     is_leaf = S > tau;
     h = is_leaf ? tau : S;
     tc = tau - S;
   }
 
   /* Brownian increment over the particle's lifetime (Eqs. green, SDE,
-   * PAPER.md:174-191): textbook Box–Muller normals.  d <= 2: one pair from
-   * block 1 (radius uniform w1:w0, angle uniform w3:w2).  d = 3 (DESIGN.md
-   * R8): two pairs — radii from block-1 words (w1:w0) and (w3:w2); angles
-   * from 32-bit uniforms: Strategy A uses block-0 word 3 and the word
-   * assembled from the 12 low bits the 53-bit uniforms leave unused (block-0
-   * w0, block-1 w0, block-1 w2); Strategy B, whose block-0 word 3 is ξ, takes
-   * both angles from block 2 (words 0 and 1).                             */
+   * PAPER.md:174-191): Box–Muller normals r·(cos, sin)(2πa).  Strategy A
+   * (R29): r = sqrt(2e) with e the Exp(1) variates split off the clock's
+   * Gamma variate, 32-bit angles.  Strategy B (R8): textbook r = sqrt(-2 log
+   * u) — d <= 2: one pair from block 1 (u = w1:w0, angle w3:w2); d = 3:
+   * radii from block-1 (w1:w0), (w3:w2), angles from block 2 (w0, w1), its
+   * block-0 word 3 being ξ.                                               */
   double xi[3];
-  if (p->dim <= 2) {
-    double v1 = or_unif53(r1[0], r1[1]), v2 = or_unif53(r1[2], r1[3]);
-    double rr = sqrt(-2.0 * log(v1));
-    xi[0] = rr * cos(2.0 * M_PI * v2);
-    xi[1] = rr * sin(2.0 * M_PI * v2);
-  } else {
-    double v1 = or_unif53(r1[0], r1[1]), v3 = or_unif53(r1[2], r1[3]);
-    double v2, v4;
-    if (strat_b) {
-      draw(c->seed, c->i, c->j, label, 2, r2);
-      v2 = or_unif32(r2[0]);
-      v4 = or_unif32(r2[1]);
+  if (strat_b) {
+    if (p->dim <= 2) {
+      double v1 = or_unif53(r1[0], r1[1]), v2 = or_unif53(r1[2], r1[3]);
+      double rr = sqrt(-2.0 * log(v1));
+      xi[0] = rr * cos(2.0 * M_PI * v2);
+      xi[1] = rr * sin(2.0 * M_PI * v2);
     } else {
-      uint32_t w4 = ((r0[0] & 0xFFFu) << 20) | ((r1[0] & 0xFFFu) << 8) | ((r1[2] & 0xFFFu) >> 4);
-      v2 = or_unif32(r0[3]);
-      v4 = or_unif32(w4);
+      double v1 = or_unif53(r1[0], r1[1]), v3 = or_unif53(r1[2], r1[3]);
+      draw(c->seed, c->i, c->j, label, 2, r2);
+      double v2 = or_unif32(r2[0]), v4 = or_unif32(r2[1]);
+      double rr = sqrt(-2.0 * log(v1));
+      xi[0] = rr * cos(2.0 * M_PI * v2);
+      xi[1] = rr * sin(2.0 * M_PI * v2);
+      xi[2] = sqrt(-2.0 * log(v3)) * cos(2.0 * M_PI * v4);
     }
-    double rr = sqrt(-2.0 * log(v1));
-    xi[0] = rr * cos(2.0 * M_PI * v2);
-    xi[1] = rr * sin(2.0 * M_PI * v2);
-    xi[2] = sqrt(-2.0 * log(v3)) * cos(2.0 * M_PI * v4);
+  } else {
+    /* angles 2π·unif32: block-1 word 0 (d <= 2); block-0 word 3 and
+     * block-1 word 3 (d = 3) */
+    double rr = sqrt(2.0 * e1);
+    double a1 = or_unif32(p->dim <= 2 ? r1[0] : r0[3]);
+    xi[0] = rr * cos(2.0 * M_PI * a1);
+    xi[1] = rr * sin(2.0 * M_PI * a1);
+    if (p->dim == 3) xi[2] = sqrt(2.0 * e2) * cos(2.0 * M_PI * or_unif32(r1[3]));
   }
   double step = nz->sigma * sqrt(h);
   double x[3];

@@ -450,78 +450,89 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       const double Sf = unif53(r0.x, r0.y);
       h2d = (leaf ? tau : tau * Sf) * P.two_d;
       tc = tau * (1.0 - Sf);
+      // Brownian increment: textbook Box–Muller from 53-bit uniforms (R8)
+      if constexpr (DIM <= 2) {
+        const double v1 = unif53(r1.x, r1.y), v2 = unif53(r1.z, r1.w);
+        const double rad = sqrt_pos(-2.0 * log_tab(v1, ltab) * h2d);
+        if constexpr (DIM == 1) {
+          y[0] = fma(rad, cospi2(2.0 * v2), y[0]);
+        } else {
+          double sn, cs;
+          sincospi2(2.0 * v2, sn, cs);
+          y[0] = fma(rad, cs, y[0]);
+          y[1] = fma(rad, sn, y[1]);
+        }
+      } else {                                   // block-0 word 3 is ξ: angles from block 2
+        const uint4 r2 = philox4x32_10(tj, c1, c2, c3 | (2u << 24), P.rk);
+        const double rad = sqrt_pos(-2.0 * log_tab(unif53(r1.x, r1.y), ltab) * h2d);
+        double sn, cs;
+        sincos2pi_u32(r2.x, sn, cs);
+        y[0] = fma(rad, cs, y[0]);
+        y[1] = fma(rad, sn, y[1]);
+        const double rad2 = sqrt_pos(-2.0 * log_tab(unif53(r1.z, r1.w), ltab) * h2d);
+        y[2] = fma(rad2, cos2pi_u32(r2.y), y[2]);
+      }
     } else {
+      // The exponential clock and the Box–Muller radii from ONE log (DESIGN.md
+      // R29): G = −ln(U_1⋯U_{m+1}) ~ Gamma(m+1), split by the spacings of m
+      // sorted uniforms into m+1 iid Exp(1) — e0 the clock's, e1 (and e2 for
+      // d = 3) the radii's (r² = 2e).  d ≤ 2: U1, U2, the spacing uniform and
+      // the offspring draw from block 0, the angle word from block 1;
+      // d = 3: U3, the two spacing uniforms and the second angle from block 1.
+      const double u12 = unif32(r0.x) * unif32(r0.y);
+      double e0, e1, e2 = 0.0;
+      if constexpr (DIM <= 2) {
+        const double v = unif32(r0.w);
+        const double G = -log_tab(u12, ltab);
+        e0 = G * v;
+        e1 = G * (1.0 - v);
+      } else {
+        const double v1 = unif32(min(r1.y, r1.z)), v2 = unif32(max(r1.y, r1.z));
+        const double G = -log_tab(u12 * unif32(r1.x), ltab);
+        e0 = G * v1;
+        e1 = G * (v2 - v1);                     // (0 when the two words tie)
+        e2 = G * (1.0 - v2);
+      }
       // exponential clock S ~ λ e^{-λS}
-      const double S = -log_tab(unif53(r0.x, r0.y), ltab) * P.inv_lambda;
+      const double S = e0 * P.inv_lambda;
       leaf = S > tau;                           // 1{S > t}
       h2d = (leaf ? tau : S) * P.two_d;         // variance 2D·h of the increment
       tc = tau - S;
-    }
-    if constexpr (F32) {
-      // the same draws and formula in single precision, on the MUFU
-      // approximations (lg2, sin/cos at |x| <= π, rsqrt seeds: ~2^-21)
-      constexpr float k2Pi = 6.28318530717958648f, kPi = 3.14159265358979324f;
-      const float hf = static_cast<float>(h2d);
-      const float v1 = static_cast<float>(unif53(r1.x, r1.y));
-      if constexpr (DIM <= 2) {
-        const float v2 = static_cast<float>(unif53(r1.z, r1.w));
-        const float rad = __fsqrt_rn(-2.0f * __logf(v1) * hf);
+      if constexpr (F32) {
+        // the same variates in single precision on the MUFU approximations
+        // (sin/cos at |x| <= π, sqrt: ~2^-21)
+        constexpr float k2Pi = 6.28318530717958648f, kPi = 3.14159265358979324f;
+        const float hf = static_cast<float>(h2d);
+        const float rad = __fsqrt_rn(2.0f * static_cast<float>(e1) * hf);
         // cos(2πv) = −cos(2πv − π), sin(2πv) = −sin(2πv − π), argument in [−π, π)
         if constexpr (DIM == 1) {
-          y[0] = fmaf(-rad, __cosf(fmaf(k2Pi, v2, -kPi)), y[0]);
+          y[0] = fmaf(-rad, __cosf(fmaf(k2Pi, static_cast<float>(unif32(r1.x)), -kPi)), y[0]);
         } else {
           float sn, cs;
-          __sincosf(fmaf(k2Pi, v2, -kPi), &sn, &cs);
+          __sincosf(fmaf(k2Pi, static_cast<float>(unif32(DIM == 2 ? r1.x : r0.w)), -kPi), &sn, &cs);
           y[0] = fmaf(-rad, cs, y[0]);
           y[1] = fmaf(-rad, sn, y[1]);
+          if constexpr (DIM == 3) {
+            const float rad2 = __fsqrt_rn(2.0f * static_cast<float>(e2) * hf);
+            y[2] = fmaf(-rad2, __cosf(fmaf(k2Pi, static_cast<float>(unif32(r1.w)), -kPi)), y[2]);
+          }
         }
+      } else if constexpr (DIM == 1) {          // the cosine normal only
+        y[0] = fma(sqrt_pos(2.0 * e1 * h2d), cos2pi_u32(r1.x), y[0]);
+      } else if constexpr (DIM == 2) {
+        const double rad = sqrt_pos(2.0 * e1 * h2d);
+        double sn, cs;
+        sincos2pi_u32(r1.x, sn, cs);
+        y[0] = fma(rad, cs, y[0]);
+        y[1] = fma(rad, sn, y[1]);
       } else {
-        const float v2 = static_cast<float>(unif32(r0.w));
-        const float v3 = static_cast<float>(unif53(r1.z, r1.w));
-        const uint32_t w4 = ((r0.x & 0xFFFu) << 20) | ((r1.x & 0xFFFu) << 8) | ((r1.z & 0xFFFu) >> 4);
-        const float v4 = static_cast<float>(unif32(w4));
-        const float rad = __fsqrt_rn(-2.0f * __logf(v1) * hf);
-        float sn, cs;
-        __sincosf(fmaf(k2Pi, v2, -kPi), &sn, &cs);
-        y[0] = fmaf(-rad, cs, y[0]);
-        y[1] = fmaf(-rad, sn, y[1]);
-        y[2] = fmaf(-__fsqrt_rn(-2.0f * __logf(v3) * hf), __cosf(fmaf(k2Pi, v4, -kPi)), y[2]);
+        const double rad = sqrt_nr(2.0 * e1 * h2d);   // (e1 may be 0)
+        double sn, cs;
+        sincos2pi_u32(r0.w, sn, cs);
+        y[0] = fma(rad, cs, y[0]);
+        y[1] = fma(rad, sn, y[1]);
+        y[2] = fma(sqrt_pos(2.0 * e2 * h2d), cos2pi_u32(r1.w), y[2]);
       }
-    } else
-    if constexpr (DIM == 1) {                   // the cosine normal only
-      const double v1 = unif53(r1.x, r1.y), v2 = unif53(r1.z, r1.w);
-      const double rad = sqrt_pos(-2.0 * log_tab(v1, ltab) * h2d);
-      y[0] = fma(rad, cospi2(2.0 * v2), y[0]);
-    } else if constexpr (DIM == 2) {
-      const double v1 = unif53(r1.x, r1.y), v2 = unif53(r1.z, r1.w);
-      const double rad = sqrt_pos(-2.0 * log_tab(v1, ltab) * h2d);
-      double sn, cs;
-      sincospi2(2.0 * v2, sn, cs);
-      y[0] = fma(rad, cs, y[0]);
-      y[1] = fma(rad, sn, y[1]);
-    } else {
-      // d = 3 from the same two blocks (R8): radii uniforms from
-      // block-1 (w1:w0), (w3:w2); angles from 32-bit uniforms — block-0 w3 and
-      // the word of the 12 low bits the 53-bit uniforms leave unused
-      const double v1 = unif53(r1.x, r1.y);
-      const double v3 = unif53(r1.z, r1.w);
-      // (angles 2π·unif32(w), reduced on the integer word: rt_math.cuh)
-      uint32_t w2, w4;
-      if constexpr (SB) {                        // block-0 word 3 is ξ: angles from block 2
-        const uint4 r2 = philox4x32_10(tj, c1, c2, c3 | (2u << 24), P.rk);
-        w2 = r2.x;
-        w4 = r2.y;
-      } else {
-        w4 = ((r0.x & 0xFFFu) << 20) | ((r1.x & 0xFFFu) << 8) | ((r1.z & 0xFFFu) >> 4);
-        w2 = r0.w;
-      }
-      const double rad = sqrt_pos(-2.0 * log_tab(v1, ltab) * h2d);
-      double sn, cs;
-      sincos2pi_u32(w2, sn, cs);
-      y[0] = fma(rad, cs, y[0]);
-      y[1] = fma(rad, sn, y[1]);
-      const double rad2 = sqrt_pos(-2.0 * log_tab(v3, ltab) * h2d);
-      y[2] = fma(rad2, cos2pi_u32(w4), y[2]);
     }
     // categorical offspring choice from the integer thresholds (R9)
     // (thresholds past the support are 0xffffffff, so the sum needs no bound)

@@ -116,3 +116,22 @@ def test_box_muller_multid(orc, dim):
     leaf = rec["ne"] == 0
     r2 = -s * s * np.log(rec["C"][leaf]) / (2 * D * t)
     assert stats.kstest(r2, stats.chi2(dim).cdf).pvalue > 1e-3
+
+
+@pytest.mark.parametrize("dim", [1, 2, 3])
+def test_clock_and_radii_independent(orc, dim):
+    """DESIGN.md R29 draws the clock and the Box–Muller radii from ONE Gamma
+    variate split by uniform spacings; they must still be independent.  With
+    λ = 1 and t = 1 a root particle is a leaf iff its clock exceeds t
+    (probability e^{-1}); among those leaves the displacement must remain
+    sqrt(2Dt) ξ with |ξ|² ~ chi-square(d) — a radius correlated with the
+    clock (e.g. sharing e0) would be inflated exactly on this event."""
+    D, t, s = 0.5, 1.0, 3.0
+    eq = dict(dim=dim, D=D, degree=1, b=[0.0, -1.0] + [0.0] * 7, lam=0.0, offspring=0,
+              init_kind=2, init_amp=1.0, init_scale=s, K=4)
+    rec = orc.trees(eq, np.zeros((1, dim)), t, 60_000, seed=17 + dim)[0]
+    leaf = rec["ne"] == 0
+    p = math.exp(-t)
+    assert abs(leaf.mean() - p) < 4 * math.sqrt(p * (1 - p) / len(leaf))
+    r2 = -s * s * np.log(rec["C"][leaf]) / (2 * D * t)
+    assert stats.kstest(r2, stats.chi2(dim).cdf).pvalue > 1e-3
