@@ -2,9 +2,9 @@
 //
 // One lane = one tree at a time; one warp = a dynamic stream of tasks (T
 // consecutive trees of one node, fetched with one atomicAdd each).  Each loop iteration advances EVERY lane by exactly one particle, so
-// the expensive part of an iteration (2 Philox blocks, logs, Box–Muller,
-// sqrt — PAPER.md:197-204 exponential clock, PAPER.md:174-191 Brownian
-// increment) runs with all 32 lanes converged whatever the trees look like;
+// the expensive part of an iteration (2 Philox blocks, one log for the clock
+// and the Box–Muller radii, sincos, sqrt — PAPER.md:197-204 exponential
+// clock, PAPER.md:174-191 Brownian increment) runs with all 32 lanes converged whatever the trees look like;
 // the tree logic after it is short predicated straight-line code.  A lane
 // whose tree ends takes the next tree of the warp's stream in the same
 // iteration (ballot + popc rank), so no lane idles until the stream runs dry.
@@ -43,8 +43,8 @@
 #include "rt_math.cuh"
 
 // Debug build (librt_debug.so, -DRT_DEBUG_BOUNDS): device bounds checks on
-// every computed index into the stack pool, free lists, overflow area, ring,
-// shared-tree slots and partials — the GPU pool offers no compute-sanitizer,
+// every computed index into the stack pool, free lists, overflow area,
+// lane-private bin sums, shared-tree slots and partials — the GPU pool offers no compute-sanitizer,
 // so the parity tests are re-run against this build (tests/test_gpu_bounds.py).
 #if defined(RT_DEBUG_BOUNDS)
 #define RT_CHECK(c)                                                              \
@@ -347,8 +347,6 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     active = true;
   };
 
-  // Transpose the pending records into the bin sums: lane b owns bin b and
-  // accumulates, in ring order, ΣC, ΣC², count of the records of bin b.
   // All trees of the task are recorded: write its partials (lane b = bin b),
   // fold the event counters, fetch the next task and start its first trees.
   auto close_and_next = [&]() {
