@@ -104,8 +104,26 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.nvml = []          # (sm MHz, reasons bitmask) every ~2 ms through NVML
+        self._stop = None
+
+    def _poll_nvml(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            while not self._stop.is_set():
+                self.nvml.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                  pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                self._stop.wait(0.002)
+        except Exception:  # noqa: BLE001 — clocks are diagnostics only
+            pass
 
     def __enter__(self):
+        import threading
+        self._stop = threading.Event()
+        self._thread = threading.Thread(target=self._poll_nvml, daemon=True)
+        self._thread.start()
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
@@ -116,6 +134,8 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
+        self._stop.set()
+        self._thread.join(timeout=5)
         self.out = ""
         if self.proc is not None:
             self.proc.terminate()
@@ -139,7 +159,26 @@ class ClockSampler:
             for nm, v in zip(names, r[5:9]):
                 if v.strip().lower() == "active":
                     reasons.add(nm)
-        if not sm:   # timed region shorter than the sampling interval: all samples
+        if not sm and self.nvml:
+            # timed region shorter than nvidia-smi's start-up: NVML samples
+            # taken every ~2 ms inside it (SM clock, clock-event reasons)
+            bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                    "sw_power_cap": 0x4}
+            sm = [float(c) for c, _ in self.nvml]
+            for _, r in self.nvml:
+                for nm, b in bits.items():
+                    if r & b:
+                        reasons.add(nm)
+            if not mx:
+                try:
+                    import pynvml
+                    mx = float(pynvml.nvmlDeviceGetMaxClockInfo(
+                        pynvml.nvmlDeviceGetHandleByIndex(self.index), pynvml.NVML_CLOCK_SM))
+                except Exception:  # noqa: BLE001
+                    pass
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx or None, "reasons": sorted(reasons),
+                    "samples": len(sm), "samples_under_load": len(sm), "source": "nvml (2 ms)"}
+        if not sm:   # no usable sample at all: every row
             sm = [float(r[1]) for r in rows if len(r) > 1 and r[1].strip().replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
                 "reasons": sorted(reasons), "samples": len(rows), "samples_under_load": len(sm)}
