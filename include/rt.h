@@ -165,7 +165,12 @@ rt_status rt_destroy(rt_handle* h);
  * standard errors se_n = sqrt(max(0, ΣC_n²/N − c_n²)/(N−1)), n = 0..K, where
  * N = n_trees counts pruned trees (R4, R11).
  * RT_E_ARG on: null pointers, n_points < 1, t <= 0 or non-finite, n_trees < 2
- * or > 2^32, non-finite points.  Times the copies inside rt_stats.total_ms. */
+ * or > 2^32, non-finite points.  Times the copies inside rt_stats.total_ms.
+ * Tree j of node i draws Philox4x32-10 blocks keyed by (seed; j, i, particle
+ * label, call), mapped to its clock and Gaussian increments as DESIGN.md R29
+ * (Strategy A: one Gamma variate split into the clock and the Box-Muller
+ * radii) or R8 (Strategy B) specify: results are reproducible bit for bit
+ * across runs and launch grids. */
 rt_status rt_estimate(rt_handle* h, const double* points, int64_t n_points, double t,
                       int64_t n_trees, uint64_t seed,
                       double* out_coeffs, double* out_stderr);
