@@ -37,3 +37,33 @@ def test_shared_trees_credit_the_walk_once():
     # independent trees: no scaling whatever n_points says
     eq0 = W.get("cfg4")["eq"]
     assert bench.algo_fp64_ops(eq0, st, n) == bench.algo_fp64_ops(eq0, st)
+
+
+def test_cost_model_strategies():
+    """Strategy B replaces the clock's log by two plain ops and adds η(τ) = τ
+    per split and 1/q per leaf; Strategy A's shift adds e^{(k-1)λτ_c} per split
+    and the root factor per tree."""
+    base = W.get("ex1A")["eq"]
+    ua = bench.algo_fp64_per_unit(base)                       # shift
+    ub = bench.algo_fp64_per_unit(W.get("ex1B")["eq"])        # Strategy B
+    up = bench.algo_fp64_per_unit(dict(base, strategy=0))     # potential
+    assert up["particle"] - ub["particle"] == 20 - 2
+    assert ua["split"] == up["split"] + 15 + 2 and ua["tree"] == up["tree"] + 1
+    assert ub["split"] == up["split"] + 1 and ub["leaf"] == up["leaf"] + 1
+
+
+def test_clock_summary_from_nvidia_smi_rows():
+    """The clocks object: median SM clock over samples under load, the
+    throttle reasons seen, and NVML samples when nvidia-smi had none."""
+    c = bench.ClockSampler(0)
+    c.out = ("0, 1965, 1965, 950.1, 0x0, Not Active, Not Active, Not Active, Not Active\n"
+             "0, 1950, 1965, 940.0, 0x4, Not Active, Not Active, Not Active, Active\n"
+             "0, 1965, 1965, 120.0, 0x1, Not Active, Not Active, Not Active, Not Active\n")
+    s = c.summary()
+    assert s["sm_mhz"] == 1957.5 and s["sm_max_mhz"] == 1965.0
+    assert s["reasons"] == ["sw_power_cap"] and s["samples_under_load"] == 2
+    c2 = bench.ClockSampler(0)
+    c2.out = ""
+    c2.nvml = [(1965, 0), (1965, 0x40), (1950, 0)]
+    s2 = c2.summary()
+    assert s2["sm_mhz"] == 1965.0 and s2["reasons"] == ["hw_thermal_slowdown"] and s2["source"].startswith("nvml")
