@@ -36,7 +36,7 @@ class Params(C.Structure):
                 ("init_scale", C.c_double), ("K", C.c_int32), ("precision", C.c_int32),
                 ("strategy", C.c_int32), ("q", C.c_double), ("coef_kind", C.c_int32 * 9),
                 ("coef_axis", C.c_int32), ("coef_scale", C.c_double), ("coef_t0", C.c_double),
-                ("shared", C.c_int32)]
+                ("shared", C.c_int32), ("sampling", C.c_int32)]
 
 
 class Norm(C.Structure):
@@ -106,6 +106,7 @@ def params(eq: dict) -> Params:
     p.coef_axis = eq.get("coef_axis", 0); p.coef_scale = eq.get("coef_scale", 1.0)
     p.coef_t0 = eq.get("coef_t0", 0.1)
     p.shared = eq.get("shared", 0)
+    p.sampling = eq.get("sampling", 0)
     return p
 
 

@@ -74,6 +74,8 @@ int or_normalize(const or_params* p, or_norm* o) {
   memset(o, 0, sizeof(*o));
   if (p->degree < 0 || p->degree > 8) return 1;
   if (p->strategy < 0 || p->strategy > 2) return 3;
+  if (p->sampling != 0 && p->sampling != 1) return 7;
+  if (p->sampling == 1 && p->strategy == 2) return 7;   /* Strategy B keeps R8 */
   double lam = p->lambda;
   /* strategy 0: λ = -b_1 if b_1 < 0 else 1 (R3); Strategy A's shift
    * u = v e^{t} uses rate 1 unless overridden            */
@@ -208,6 +210,14 @@ static double particle(tree_ctx* c, const double* y, double tau, uint64_t label)
     double Sf = or_unif53(r0[0], r0[1]);               /* S ~ U(0,1) */
     h = is_leaf ? tau : tau * Sf;
     tc = tau * (1.0 - Sf);
+  } else if (p->sampling == 1) {
+    /* textbook sampling (pin of R29 in law, see rt_oracle.h): the clock by
+     * inversion, S = -ln(u)/λ; the normals below by
+     * Box–Muller with r = sqrt(-2 ln v)                                    */
+    double S = -log(or_unif53(r0[0], r0[1])) * nz->inv_lambda;
+    is_leaf = S > tau;
+    h = is_leaf ? tau : S;
+    tc = tau - S;
   } else {
     /* DESIGN.md R29: G = -log(U_1 ... U_{m+1}) ~ Gamma(m+1) split by the
      * spacings of m sorted uniforms into m+1 iid Exp(1) variates: e0 for the
@@ -241,7 +251,17 @@ static double particle(tree_ctx* c, const double* y, double tau, uint64_t label)
    * radii from block-1 (w1:w0), (w3:w2), angles from block 2 (w0, w1), its
    * block-0 word 3 being ξ.                                               */
   double xi[3];
-  if (strat_b) {
+  if (!strat_b && p->sampling == 1) {
+    double v1 = or_unif53(r1[0], r1[1]), v2 = or_unif53(r1[2], r1[3]);
+    double rr = sqrt(-2.0 * log(v1));
+    xi[0] = rr * cos(2.0 * M_PI * v2);
+    xi[1] = rr * sin(2.0 * M_PI * v2);
+    if (p->dim == 3) {
+      draw(c->seed, c->i, c->j, label, 2, r2);
+      double v3 = or_unif53(r2[0], r2[1]), v4 = or_unif53(r2[2], r2[3]);
+      xi[2] = sqrt(-2.0 * log(v3)) * cos(2.0 * M_PI * v4);
+    }
+  } else if (strat_b) {
     if (p->dim <= 2) {
       double v1 = or_unif53(r1[0], r1[1]), v2 = or_unif53(r1[2], r1[3]);
       double rr = sqrt(-2.0 * log(v1));

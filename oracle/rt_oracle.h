@@ -46,6 +46,15 @@ typedef struct {
                            the node index, every node sees the same trees, node
                            i's leaves are evaluated at x_i + δ (δ the leaf's
                            displacement from the root); constant coefficients */
+  int32_t sampling;     /* Strategy A only.  0: the contract (R29: one
+                           Gamma(m+1) variate split by uniform spacings into the
+                           clock and the Box–Muller radii, 32-bit uniforms).
+                           1: TEXTBOOK sampling, a pin of R29 in law only
+                           (tests/test_oracle_sampling.py): S = -ln(u)/λ with
+                           u = unif53(call-0 w1:w0), Box–Muller r = sqrt(-2 ln v1),
+                           angle 2π v2 from the unif53 pair of call 1 (call 2
+                           for the third normal, d = 3) — SURVEY.md §8(c)'s
+                           original definition.  Never the product's contract. */
 } or_params;
 
 typedef struct {

@@ -173,3 +173,27 @@ def fd_solve_1d_xt(fxt, g, t: float, D: float = 1.0, L: float = 12.0, dx: float 
 
 def catalan(n: int) -> int:
     return math.comb(2 * n, n) // (n + 1)
+
+
+def lorentz_heat(x, t: float, D: float, lam: float, A: float, s: float) -> np.ndarray:
+    """u for u_t = DΔu - λu, u(x,0) = A / (1 + |x|²/s²) in any dimension d.
+
+    Derived without the radial density used elsewhere: write
+    1/(1 + a) = ∫_0^∞ e^{-w(1 + a)} dw and average the Gaussian factor
+    e^{-w|X|²/s²} over X ~ N(x, 2Dt I_d) in closed form,
+    E e^{-w|X|²/s²} = (1 + 4Dtw/s²)^{-d/2} exp(-w|x|² / (s² + 4Dtw)),
+    so u = e^{-λt} A ∫_0^∞ e^{-w} (1 + 4Dtw/s²)^{-d/2}
+    exp(-w|x|²/(s² + 4Dtw)) dw (one smooth, exponentially decaying integral,
+    scipy quad)."""
+    from scipy.integrate import quad
+    x = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    d = x.shape[1]
+    v = 2.0 * D * t
+    out = np.empty(x.shape[0])
+    for i, xi in enumerate(x):
+        r2 = float(np.sum(xi * xi))
+        f = lambda w: math.exp(-w) * (1.0 + 2.0 * v * w / s ** 2) ** (-d / 2.0) * \
+            math.exp(-w * r2 / (s ** 2 + 2.0 * v * w))   # noqa: E731
+        val, _ = quad(f, 0.0, math.inf, epsabs=1e-15, epsrel=1e-13, limit=400)
+        out[i] = math.exp(-lam * t) * A * val
+    return out

@@ -30,8 +30,10 @@ int main(void) {
   for (int dim = 1; dim <= 3; ++dim)
     for (int strategy = 0; strategy <= 2; ++strategy)
       for (int kind = 0; kind <= 3; ++kind)
-        for (int shared = 0; shared <= 1; ++shared) {
+        for (int shared = 0; shared <= 1; ++shared)
+        for (int sampling = 0; sampling <= (strategy == 2 ? 0 : 1); ++sampling) {
           or_params p = base(dim, strategy, kind, shared);
+          p.sampling = sampling;   /* 1: the textbook sampler (pin of R29 in law) */
           or_stats st;
           if (or_sums(&p, pts, 4, 1.0, 7, 200, 3, sums, &st)) bad++;
           if (or_trees(&p, pts, 4, 0.5, 0, 50, 11, rec)) bad++;
