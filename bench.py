@@ -338,7 +338,7 @@ def main():
             walk[1].record(cur)
         merge_sums(sums)                     # one all-reduce of (K+2)x3 doubles per node
         c, se, us, ses = P.finalize(sums, K, N * ws)
-        u, fl = P.pade(c, L, M)
+        u, fl = P.pade(c, L, M, se_sum=ses)
         return u, ses
 
     for _ in range(args.warmup):
@@ -420,22 +420,49 @@ def main():
 
     # ---- end to end through the public host API (rt_interface_values) -----
     e2e = None
-    if cfg["nodes"]["kind"] == "planes":
+    if ws > 1:
+        # N ranks: each rank's host points go up, it samples ITS tree range
+        # (rt_sums_dev(tree_offset)), the sums are merged by one all-reduce,
+        # every rank finalises + resums the merged series and reads back u and
+        # its standard error — the sharded job end to end
+        pin = torch.as_tensor(pts).pin_memory()
+        out_u = torch.empty(n, dtype=torch.float64).pin_memory()
+        out_se = torch.empty_like(out_u).pin_memory()
+
+        def e2e_step():
+            xd = pin.to("cuda", non_blocking=True)
+            s_ = est.sums(xd, t, n_rank, seed, tree_offset=off)
+            merge_sums(s_)
+            c_, _, _, ses_ = P.finalize(s_, K, N * ws)
+            u_, _ = P.pade(c_, L, M, se_sum=ses_)
+            out_u.copy_(u_, non_blocking=True)
+            out_se.copy_(ses_, non_blocking=True)
+            torch.cuda.synchronize()
+
+        e2e_step()
+        dist.barrier()
+        t0 = time.perf_counter()
+        e2e_steps = max(1, min(args.steps, 3))
+        for _ in range(e2e_steps):
+            e2e_step()
+        e2e_s = time.perf_counter() - t0
+        tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = tt.item()
+        e2e = {"value": n * N * ws * e2e_steps / e2e_s, "unit": "trees/s",
+               "h2d_bytes_per_step": n * eq["dim"] * 8, "d2h_bytes_per_step": 2 * n * 8,
+               "api": "per rank: host points -> rt_sums_dev(tree range) -> all-reduce -> "
+                      "rt_finalize_dev -> rt_pade_dev -> host (u, se)"}
+    elif cfg["nodes"]["kind"] == "planes":
         planes = cfg["nodes"]["planes"]
         est.interface_values(planes, n, t, N, seed, L, M)          # warm
-        if dist is not None:
-            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e2e_steps = max(1, min(args.steps, 3))
         for _ in range(e2e_steps):
             est.interface_values(planes, n, t, N, seed, L, M)
         e2e_s = time.perf_counter() - t0
-        if dist is not None:
-            tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = tt.item()
-        e2e = {"value": n * N * ws * e2e_steps / e2e_s, "unit": "trees/s",
+        e2e = {"value": n * N * e2e_steps / e2e_s, "unit": "trees/s",
                "h2d_bytes_per_step": n * eq["dim"] * 8,
                "d2h_bytes_per_step": n * eq["dim"] * 8 + n * 8 * 2 + n * 4,
                "api": "rt_interface_values (host buffers; node placement, walk, Padé, copies)"}

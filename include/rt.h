@@ -50,7 +50,8 @@ typedef enum {
   RT_E_ARG = 1,     /* invalid argument (null pointer, out-of-range value) */
   RT_E_CUDA = 2,    /* CUDA runtime error (message in rt_last_error)        */
   RT_E_NOMEM = 3,   /* device allocation failed                            */
-  RT_E_STATE = 4    /* handle state error                                  */
+  RT_E_STATE = 4,   /* handle state error                                  */
+  RT_E_NUMERIC = 5  /* a result is not finite (rt_pdd_solve's nodal values) */
 } rt_status;
 
 /* Offspring law for the branching power α. */
@@ -198,13 +199,24 @@ rt_status rt_finalize_dev(const double* d_sums, int64_t n_points, int32_t K, int
 /* [L/M] Padé at z = 1 of each node's c_0..c_{L+M} (row stride K+1):
  * Q(0) = 1, deg P <= L, deg Q <= M, Q Σc_n z^n − P = O(z^{L+M+1}), denominator
  * by Gaussian elimination with partial pivoting.
- * out_u [n_points]; out_flags [n_points] (may be NULL): bit0 zero pivot (u =
- * NaN), bit1 |Q(1)| <= 1e-14 |P(1)|, bit2 Q has a sign change on (0, 1].
- * RT_E_ARG: null pointers, n_points < 1, L < 0, M < 0, M > 16, L + M > K. */
+ * out_u [n_points]; out_flags [n_points] (may be NULL):
+ *   bit0  exact zero pivot in [L/M] (degenerate table): u is the value of the
+ *         largest regular [L/M'], M' < M — [L/0] = c_0+…+c_L always is —
+ *         SPEC.md:403's fallback; M' is stored in bits 8..15;
+ *   bit1  |Q(1)| <= 1e-14 |P(1)|;
+ *   bit2  Q has a sign change on (0, 1] (256 equispaced points);
+ *   bit3  |u − Σ_{n=0}^{K} c_n| > 10 se_sum[i] — the resummed value and the
+ *         partial sum disagree beyond the statistics;
+ *         only when se_sum [n_points] (the standard error of the partial sum,
+ *         rt_finalize_dev's d_se_sum) is given, else never set.
+ * u is NaN only for non-finite coefficients.  One warp per node, all in
+ * registers.  RT_E_ARG: null coeffs/out_u, n_points < 1, L < 0, M < 0,
+ * M > 16, L + M > K, K > 30.  Host variant synchronous; _dev stream-ordered. */
 rt_status rt_pade(const double* coeffs, int64_t n_points, int32_t K, int32_t L, int32_t M,
-                  double* out_u, uint32_t* out_flags);
+                  const double* se_sum, double* out_u, uint32_t* out_flags);
 rt_status rt_pade_dev(const double* d_coeffs, int64_t n_points, int32_t K, int32_t L,
-                      int32_t M, double* d_u, uint32_t* d_flags, void* stream);
+                      int32_t M, const double* d_se_sum, double* d_u, uint32_t* d_flags,
+                      void* stream);
 
 /* Row a9: place nodes on planes (plane-major; free axes row-major ascending;
  * linspace(lo, hi, n) = lo + (hi−lo)·(j/(n−1)); exact duplicates of earlier
@@ -285,7 +297,9 @@ rt_status rt_pdd_downstream_dev(rt_handle* h, const rt_pdd_cfg* cfg, const doubl
 
 /* The whole PDD (synchronous, host buffers): nodal values by the tree walk,
  * splines, subdomain solves.  out_nodal [6][n_t][n_s] and out_ms[3] = {T_MC,
- * T_INT, T_LOCAL} (device time, ms) may be NULL. */
+ * T_INT, T_LOCAL} (device time, ms) may be NULL.  A degenerate Padé table at
+ * a nodal point falls back to a lower order (rt_pade bit0); RT_E_NUMERIC if a
+ * nodal value is still not finite (the field is then not computed). */
 rt_status rt_pdd_solve(rt_handle* h, const rt_pdd_cfg* cfg, double* out_field, double* out_nodal,
                        double* out_ms);
 

@@ -84,6 +84,8 @@ def lib():
         _lib.or_finalize.argtypes = [dp, C.c_int64, C.c_int32, C.c_int64, dp, dp, dp, dp]
         _lib.or_finalize.restype = None
         _lib.or_pade.argtypes = [dp, C.c_int32, C.c_int32, dp, C.POINTER(C.c_uint32), dp, dp]
+        _lib.or_pade_node.argtypes = [dp, C.c_int32, C.c_int32, C.c_int32, C.c_double, dp,
+                                      C.POINTER(C.c_uint32)]
     return _lib
 
 
@@ -213,3 +215,13 @@ def pade(c, L: int, M: int):
     if e:
         raise ValueError(f"or_pade error {e}")
     return u.value, fl.value, p, q
+
+
+def pade_node(c, K: int, L: int, M: int, se_sum: float):
+    """[L/M] Padé at z = 1 with the bit3 divergence flag -> (u, flags)."""
+    cc = np.ascontiguousarray(np.asarray(c, dtype=np.float64))
+    u = C.c_double(); fl = C.c_uint32()
+    e = lib().or_pade_node(_dp(cc), K, L, M, float(se_sum), C.byref(u), C.byref(fl))
+    if e:
+        raise ValueError(f"or_pade_node error {e}")
+    return u.value, fl.value

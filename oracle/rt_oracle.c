@@ -450,13 +450,15 @@ void or_finalize(const double* sums, int64_t n_points, int32_t K, int64_t N,
  * deg Q <= M, Q(0) = 1 and Q(z) Σ c_n z^n - P(z) = O(z^{L+M+1}).  The
  * denominator solves Σ_{j=1..M} q_j c_{L+i-j} = -c_{L+i}, i = 1..M (c_{<0} = 0),
  * by Gaussian elimination with partial pivoting; p_i = Σ_{j<=min(i,M)} q_j c_{i-j}.
- * Evaluated at z = 1 (the series variable counts splitting events; R4). */
-int or_pade(const double* c, int32_t L, int32_t M, double* u, uint32_t* flags,
-            double* p_out, double* q_out) {
+ * Evaluated at z = 1 (the series variable counts splitting events; R4).
+ *
+ * Degenerate table ("falls back to highest non-degenerate order,
+ * flagged"; R12): if the [L/M] system has an exact zero pivot, the
+ * value is that of [L/M'] for the largest M' < M whose system is regular —
+ * [L/0], the partial sum c_0 + … + c_L, always is — bit0 is set and M' is
+ * stored in flag bits 8..15.                                                */
+static int pade_denominator(const double* c, int32_t L, int32_t M, double* q) {
   double A[16][17];
-  double q[17], pc[17];
-  uint32_t fl = 0;
-  if (L < 0 || M < 0 || M > 16 || L > 16) return 1;
   q[0] = 1.0;
   for (int i = 1; i <= M; ++i) {
     for (int j = 1; j <= M; ++j) {
@@ -470,7 +472,7 @@ int or_pade(const double* c, int32_t L, int32_t M, double* u, uint32_t* flags,
     int piv = col;
     for (int r = col + 1; r < M; ++r)
       if (fabs(A[r][col]) > fabs(A[piv][col])) piv = r;
-    if (A[piv][col] == 0.0) { fl |= 1u; break; }
+    if (A[piv][col] == 0.0) return 1;                   /* exact zero pivot */
     if (piv != col)
       for (int k = 0; k <= M; ++k) { double tmp = A[col][k]; A[col][k] = A[piv][k]; A[piv][k] = tmp; }
     for (int r = col + 1; r < M; ++r) {
@@ -478,35 +480,60 @@ int or_pade(const double* c, int32_t L, int32_t M, double* u, uint32_t* flags,
       for (int k = col; k <= M; ++k) A[r][k] -= f * A[col][k];
     }
   }
-  if (fl & 1u) {
-    *u = NAN;
-    if (flags) *flags = fl;
-    return 0;
-  }
   /* back substitution */
   for (int r = M - 1; r >= 0; --r) {
     double s = A[r][M];
     for (int k = r + 1; k < M; ++k) s -= A[r][k] * q[k + 1];
     q[r + 1] = s / A[r][r];
   }
+  return 0;
+}
+
+int or_pade(const double* c, int32_t L, int32_t M, double* u, uint32_t* flags,
+            double* p_out, double* q_out) {
+  double q[17], pc[17];
+  uint32_t fl = 0;
+  if (L < 0 || M < 0 || M > 16 || L > 16) return 1;
+  int Mu = M;
+  while (Mu > 0 && pade_denominator(c, L, Mu, q)) --Mu;   /* degenerate: lower M */
+  if (Mu == 0) q[0] = 1.0;
+  if (Mu < M) fl |= 1u | ((uint32_t)Mu << 8);
+  for (int j = Mu + 1; j <= M; ++j) q[j] = 0.0;
   for (int i = 0; i <= L; ++i) {
     double s = 0.0;
-    for (int j = 0; j <= (i < M ? i : M); ++j) s += q[j] * c[i - j];
+    for (int j = 0; j <= (i < Mu ? i : Mu); ++j) s += q[j] * c[i - j];
     pc[i] = s;
   }
   double P1 = 0.0, Q1 = 0.0;
   for (int i = 0; i <= L; ++i) P1 += pc[i];
-  for (int j = 0; j <= M; ++j) Q1 += q[j];
+  for (int j = 0; j <= Mu; ++j) Q1 += q[j];
   *u = P1 / Q1;
   if (fabs(Q1) <= 1e-14 * fabs(P1)) fl |= 2u;
   /* sign change of Q on (0, 1]: Q(0) = 1; sample 256 equispaced points */
   for (int s = 1; s <= 256; ++s) {
     double z = (double)s / 256.0, Qz = 0.0, zp = 1.0;
-    for (int j = 0; j <= M; ++j) { Qz += q[j] * zp; zp *= z; }
+    for (int j = 0; j <= Mu; ++j) { Qz += q[j] * zp; zp *= z; }
     if (!(Qz > 0.0)) { fl |= 4u; break; }
   }
   if (flags) *flags = fl;
   if (p_out) for (int i = 0; i <= L; ++i) p_out[i] = pc[i];
   if (q_out) for (int j = 0; j <= M; ++j) q_out[j] = q[j];
+  return 0;
+}
+
+/* Per-node resummation with the divergence diagnostic (
+ * PAPER.md:295-301 the partial sums of a divergent series, 766-769 artificial
+ * poles): or_pade of c[0..L+M], plus bit3 when the Padé value and the partial
+ * sum u_sum = c_0 + … + c_K (the estimate whose standard error is se_sum)
+ * differ by more than 10 se_sum.                                            */
+int or_pade_node(const double* c, int32_t K, int32_t L, int32_t M, double se_sum,
+                 double* u, uint32_t* flags) {
+  uint32_t fl = 0;
+  int e = or_pade(c, L, M, u, &fl, NULL, NULL);
+  if (e) return e;
+  double us = 0.0;
+  for (int n = 0; n <= K; ++n) us += c[n];
+  if (fabs(*u - us) > 10.0 * se_sum) fl |= 8u;
+  if (flags) *flags = fl;
   return 0;
 }

@@ -109,10 +109,14 @@ int or_sums(const or_params* p, const double* points, int64_t n_points, double t
 void or_finalize(const double* sums, int64_t n_points, int32_t K, int64_t N,
                  double* coeffs, double* stderr_n, double* u_sum, double* se_sum);
 
-/* [L/M] Padé of c[0..L+M] evaluated at z = 1; flags bit0 zero pivot,
- * bit1 |Q(1)| <= 1e-14 |P(1)|, bit2 Q changes sign on (0,1]. */
+/* [L/M] Padé of c[0..L+M] evaluated at z = 1; flags bit0 zero pivot in
+ * [L/M] (the value is then [L/M'], M' < M the largest regular order, M' in
+ * bits 8..15), bit1 |Q(1)| <= 1e-14 |P(1)|, bit2 Q changes sign on (0,1]. */
 int or_pade(const double* c, int32_t L, int32_t M, double* u, uint32_t* flags,
             double* p_out, double* q_out);
+/* or_pade plus bit3: |u - (c_0 + ... + c_K)| > 10 se_sum. */
+int or_pade_node(const double* c, int32_t K, int32_t L, int32_t M, double se_sum,
+                 double* u, uint32_t* flags);
 
 #ifdef __cplusplus
 }

@@ -12,7 +12,7 @@ CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "librt.so")
 SO_DEBUG = os.path.join(HERE, "librt_debug.so")   # -DRT_DEBUG_BOUNDS (tests/test_gpu_bounds.py)
 SOURCES = [os.path.join(CSRC, "rt_api.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("tree_walk.cuh", "philox.cuh", "rt_math.cuh", "rt_math_tables.h", "pdd.cuh", "shared_eval.cuh")] + \
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("tree_walk.cuh", "philox.cuh", "rt_math.cuh", "rt_math_tables.h", "pdd.cuh", "shared_eval.cuh", "pade.cuh")] + \
     [os.path.join(ROOT, "include", "rt.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -20,6 +20,7 @@
 #include "tree_walk.cuh"
 #include "pdd.cuh"
 #include "shared_eval.cuh"
+#include "pade.cuh"
 
 using rtk::WalkParams;
 
@@ -87,6 +88,7 @@ struct rt_handle {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaStream_t last_stream = nullptr;
   bool have_timing = false;
+  bool scratch_used = false;   // ev[2] marks the last use of the scratch on last_stream
   double host_total_ms = -1.0;
   DevBuf partials, gpool, gaux, lacc, wtime, sh_tsum, sh_leaves, sh_sorted, sh_boff, pdd_pts, pdd_nodal, pdd_bc, pdd_field, pdd_c, pdd_u, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
   int32_t grid_override = 0;
@@ -328,8 +330,11 @@ static rt_status plan_launch(rt_handle* h, KernelFn fn, int smem, int64_t n_poin
   }
   T = std::min<int64_t>(T, n_trees);
   // task ids are 32-bit in the kernel: grow tasks until they number < 2^31
-  while (n_points * ((n_trees + T - 1) / T) >= (int64_t(1) << 31)) T *= 2;
-  T = std::min<int64_t>(T, n_trees);
+  // (n_points < 2^31, so T = n_trees — one task per node — always ends it)
+  while (T < n_trees && n_points * ((n_trees + T - 1) / T) >= (int64_t(1) << 31))
+    T = std::min<int64_t>(T * 2, n_trees);
+  if (n_points * ((n_trees + T - 1) / T) >= (int64_t(1) << 31))
+    return fail(RT_E_ARG, "too many tasks (n_points = %lld)", static_cast<long long>(n_points));
   L.T = T;
   L.tpn = (n_trees + T - 1) / T;
   L.n_tasks = n_points * L.tpn;
@@ -410,7 +415,7 @@ static rt_status check_run_args(const rt_handle* h, int64_t n_points, double t,
   if (tree_offset < 0 || tree_offset + n_trees > (int64_t(1) << 32))
     return fail(RT_E_ARG, "tree range must lie in [0, 2^32)");
   if (n_trees >= (int64_t(1) << 31)) return fail(RT_E_ARG, "n_trees must be < 2^31 per call");
-  if (n_points > (int64_t(1) << 31)) return fail(RT_E_ARG, "n_points too large");
+  if (n_points >= (int64_t(1) << 31)) return fail(RT_E_ARG, "n_points must be < 2^31");
   return RT_OK;
 }
 
@@ -450,6 +455,30 @@ static void fill_params(const rt_handle* h, WalkParams& P, double t, uint64_t se
   P.beta = nz.beta;
   P.K = p.K;
   P.nb = p.K + 2;
+}
+
+// The handle's scratch (partials, lane-private sums, overflow stacks, task
+// counter, PDD tables) is shared by every call: work on a stream other than
+// the one that last used it waits for that work first (ev[2] is recorded
+// after every call's last use of the scratch).  (a host call on
+// the handle's own stream after an unsynchronised _dev call raced on it.)
+// Work captured into a CUDA graph is ordered by the graph's user instead
+// (a capture may not wait on uncaptured work), so captures neither wait nor
+// leave a mark.
+static bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+
+static rt_status order_after_last(rt_handle* h, cudaStream_t st) {
+  if (h->scratch_used && h->last_stream != st && !capturing(st))
+    RT_CUDA(cudaStreamWaitEvent(st, h->ev[2], 0));
+  return RT_OK;
+}
+
+static void mark_scratch(rt_handle* h, cudaStream_t st) {
+  h->last_stream = st;
+  h->scratch_used = !capturing(st);
 }
 
 // Shared trees (NEXT row f4): phase 1 walks every tree once
@@ -567,7 +596,7 @@ static rt_status run_walk_shared(rt_handle* h, KernelFn prod, int smem, int pool
       static_cast<double*>(h->partials.p), tpn_total, nb, d_sums,
       static_cast<unsigned long long*>(h->stats.p));
   RT_CUDA(cudaGetLastError());
-  h->last_stream = st;
+  mark_scratch(h, st);
   h->have_timing = true;
   h->host_total_ms = -1.0;
   return RT_OK;
@@ -576,6 +605,10 @@ static rt_status run_walk_shared(rt_handle* h, KernelFn prod, int smem, int pool
 static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points, double t,
                           int64_t tree_offset, int64_t n_trees, uint64_t seed, int rec_shift,
                           rtk::TreeRec* d_recs, double* d_sums, cudaStream_t st) {
+  {
+    const rt_status o = order_after_last(h, st);
+    if (o != RT_OK) return o;
+  }
   const rt_eq_params& p = h->p;
   const Norm& nz = h->nz;
   int smem = 0, pool_cap = 0;
@@ -654,7 +687,7 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
       static_cast<double*>(h->partials.p), L.tpn, nb, d_sums,
       static_cast<unsigned long long*>(h->stats.p));
   RT_CUDA(cudaGetLastError());
-  h->last_stream = st;
+  mark_scratch(h, st);
   h->have_timing = true;
   h->host_total_ms = -1.0;
   return RT_OK;
@@ -790,102 +823,49 @@ extern "C" rt_status rt_estimate(rt_handle* h, const double* points, int64_t n_p
 }
 
 // ---------------------------------------------------------------------------
-// row a8: batched [L/M] Padé, one thread per node (negligible cost, M <= 16)
-__global__ void pade_kernel(const double* __restrict__ coeffs, int64_t n, int stride, int L,
-                            int M, double* __restrict__ out_u, uint32_t* __restrict__ flags) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double* c = coeffs + i * stride;
-  double A[16][17];
-  double q[17];
-  uint32_t fl = 0;
-  // Toeplitz system Σ_j q_j c_{L+r-j} = -c_{L+r}, r = 1..M
-  for (int r = 0; r < M; ++r) {
-    for (int j = 0; j < M; ++j) {
-      const int idx = L + r - j;
-      A[r][j] = idx >= 0 ? c[idx] : 0.0;
-    }
-    A[r][M] = -c[L + r + 1];
-  }
-  for (int col = 0; col < M && !(fl & 1u); ++col) {
-    int piv = col;
-    double best = fabs(A[col][col]);
-    for (int r = col + 1; r < M; ++r) {
-      const double v = fabs(A[r][col]);
-      if (v > best) { best = v; piv = r; }
-    }
-    if (best == 0.0) { fl |= 1u; break; }
-    if (piv != col)
-      for (int k = col; k <= M; ++k) { const double tmp = A[col][k]; A[col][k] = A[piv][k]; A[piv][k] = tmp; }
-    for (int r = col + 1; r < M; ++r) {
-      const double f = A[r][col] / A[col][col];
-      for (int k = col; k <= M; ++k) A[r][k] = __dsub_rn(A[r][k], __dmul_rn(f, A[col][k]));
-    }
-  }
-  if (fl & 1u) {
-    out_u[i] = __longlong_as_double(0x7ff8000000000000ll);
-    if (flags) flags[i] = fl;
-    return;
-  }
-  q[0] = 1.0;
-  for (int r = M - 1; r >= 0; --r) {
-    double s = A[r][M];
-    for (int k = r + 1; k < M; ++k) s = __dsub_rn(s, __dmul_rn(A[r][k], q[k + 1]));
-    q[r + 1] = s / A[r][r];
-  }
-  double P1 = 0.0, Q1 = 0.0;
-  for (int a = 0; a <= L; ++a) {
-    double pa = 0.0;
-    const int jm = a < M ? a : M;
-    for (int j = 0; j <= jm; ++j) pa = __dadd_rn(pa, __dmul_rn(q[j], c[a - j]));
-    P1 += pa;
-  }
-  for (int j = 0; j <= M; ++j) Q1 += q[j];
-  out_u[i] = P1 / Q1;
-  if (fabs(Q1) <= 1e-14 * fabs(P1)) fl |= 2u;
-  for (int s = 1; s <= 256; ++s) {
-    const double z = static_cast<double>(s) / 256.0;
-    double Qz = 0.0, zp = 1.0;
-    for (int j = 0; j <= M; ++j) { Qz = __dadd_rn(Qz, __dmul_rn(q[j], zp)); zp *= z; }
-    if (!(Qz > 0.0)) { fl |= 4u; break; }
-  }
-  if (flags) flags[i] = fl;
+// row a8: batched [L/M] Padé, one warp per node (pade.cuh)
+static void launch_pade(const double* d_c, int64_t n, int K, int L, int M, const double* d_se_sum,
+                        double* d_u, uint32_t* d_flags, cudaStream_t st) {
+  const int per_cta = rtk::kPadeThreads / 32;
+  rtk::pade_warp_kernel<<<static_cast<unsigned>((n + per_cta - 1) / per_cta), rtk::kPadeThreads, 0, st>>>(
+      d_c, n, K, L, M, d_se_sum, d_u, d_flags);
 }
 
 static rt_status check_pade_args(int64_t n_points, int32_t K, int32_t L, int32_t M) {
   if (n_points < 1) return fail(RT_E_ARG, "n_points must be >= 1");
-  if (L < 0 || M < 0 || M > 16 || L + M > K)
-    return fail(RT_E_ARG, "need 0 <= L, 0 <= M <= 16, L + M <= K (L=%d M=%d K=%d)", L, M, K);
+  if (L < 0 || M < 0 || M > 16 || L + M > K || K > 30)
+    return fail(RT_E_ARG, "need 0 <= L, 0 <= M <= 16, L + M <= K <= 30 (L=%d M=%d K=%d)", L, M, K);
   return RT_OK;
 }
 
 extern "C" rt_status rt_pade_dev(const double* d_coeffs, int64_t n_points, int32_t K, int32_t L,
-                                 int32_t M, double* d_u, uint32_t* d_flags, void* stream) {
+                                 int32_t M, const double* d_se_sum, double* d_u, uint32_t* d_flags,
+                                 void* stream) {
   if (!d_coeffs || !d_u) return fail(RT_E_ARG, "null pointer");
   rt_status s = check_pade_args(n_points, K, L, M);
   if (s != RT_OK) return s;
-  const unsigned blocks = static_cast<unsigned>((n_points + 127) / 128);
-  pade_kernel<<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(d_coeffs, n_points, K + 1,
-                                                                      L, M, d_u, d_flags);
+  launch_pade(d_coeffs, n_points, K, L, M, d_se_sum, d_u, d_flags, static_cast<cudaStream_t>(stream));
   RT_CUDA(cudaGetLastError());
   return RT_OK;
 }
 
 extern "C" rt_status rt_pade(const double* coeffs, int64_t n_points, int32_t K, int32_t L,
-                             int32_t M, double* out_u, uint32_t* out_flags) {
+                             int32_t M, const double* se_sum, double* out_u, uint32_t* out_flags) {
   if (!coeffs || !out_u) return fail(RT_E_ARG, "null pointer");
   rt_status s = check_pade_args(n_points, K, L, M);
   if (s != RT_OK) return s;
   const size_t cb = static_cast<size_t>(n_points) * (K + 1) * sizeof(double);
-  double *dc = nullptr, *du = nullptr;
+  double *dc = nullptr, *du = nullptr, *dse = nullptr;
   uint32_t* df = nullptr;
   RT_CUDA(cudaMalloc(&dc, cb));
   cudaError_t e = cudaMalloc(&du, n_points * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&df, n_points * sizeof(uint32_t));
+  if (e == cudaSuccess && se_sum) e = cudaMalloc(&dse, n_points * sizeof(double));
   if (e == cudaSuccess) e = cudaMemcpy(dc, coeffs, cb, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && se_sum)
+    e = cudaMemcpy(dse, se_sum, n_points * sizeof(double), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
-    pade_kernel<<<static_cast<unsigned>((n_points + 127) / 128), 128>>>(dc, n_points, K + 1, L, M,
-                                                                         du, df);
+    launch_pade(dc, n_points, K, L, M, dse, du, df, nullptr);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaMemcpy(out_u, du, n_points * sizeof(double), cudaMemcpyDeviceToHost);
@@ -894,6 +874,7 @@ extern "C" rt_status rt_pade(const double* coeffs, int64_t n_points, int32_t K, 
   cudaFree(dc);
   cudaFree(du);
   cudaFree(df);
+  cudaFree(dse);
   if (e != cudaSuccess) return fail(RT_E_CUDA, "rt_pade: %s", cudaGetErrorString(e));
   return RT_OK;
 }
@@ -976,7 +957,7 @@ extern "C" rt_status rt_interface_values(rt_handle* h, const rt_plane* planes, i
   finalize_kernel<<<static_cast<unsigned>(n), 32, 0, st>>>(d_sums, K, static_cast<double>(n_trees),
                                                             d_c, nullptr, nullptr, d_se);
   RT_CUDA(cudaGetLastError());
-  pade_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(d_c, n, K + 1, L, M, d_u, d_fl);
+  launch_pade(d_c, n, K, L, M, d_se, d_u, d_fl, st);
   RT_CUDA(cudaGetLastError());
   RT_CUDA(cudaEventRecord(h->ev[2], st));
   RT_CUDA(cudaMemcpyAsync(out_points, d_pts, pts.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1079,6 +1060,10 @@ extern "C" rt_status rt_pdd_nodes(const rt_pdd_cfg* cfg, double* out) {
 
 static rt_status pdd_downstream(rt_handle* h, const rt_pdd_cfg* cfg, const double* d_nodal,
                                 double* d_field, double* d_bc, cudaStream_t st) {
+  {
+    const rt_status o = order_after_last(h, st);
+    if (o != RT_OK) return o;
+  }
   const rtk::PddGeom G = pdd_geom(cfg);
   double* bc = d_bc;
   if (!bc) {
@@ -1106,7 +1091,12 @@ extern "C" rt_status rt_pdd_downstream_dev(rt_handle* h, const rt_pdd_cfg* cfg,
   rt_status s = check_pdd(h, cfg);
   if (s != RT_OK) return s;
   if (!d_nodal || !d_field) return fail(RT_E_ARG, "null pointer");
-  return pdd_downstream(h, cfg, d_nodal, d_field, d_bc, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  s = pdd_downstream(h, cfg, d_nodal, d_field, d_bc, st);
+  if (s != RT_OK) return s;
+  RT_CUDA(cudaEventRecord(h->ev[2], st));
+  mark_scratch(h, st);
+  return RT_OK;
 }
 
 // t_0 nodal values: g at the nodal points (no Monte Carlo at t = 0)
@@ -1168,8 +1158,9 @@ extern "C" rt_status rt_pdd_solve(rt_handle* h, const rt_pdd_cfg* cfg, double* o
     if (s != RT_OK) return s;
     finalize_kernel<<<static_cast<unsigned>(npts), 32, 0, st>>>(
         sums, K, static_cast<double>(cfg->n_trees), dc, nullptr, nullptr, nullptr);
-    pade_kernel<<<static_cast<unsigned>((npts + 127) / 128), 128, 0, st>>>(dc, npts, K + 1, cfg->L,
-                                                                          cfg->M, du, nullptr);
+    // (a degenerate table — e.g. no tree reaching L splits at an early level —
+    // falls back to the largest regular [L/M'], finite; pade.cuh bit0)
+    launch_pade(dc, npts, K, cfg->L, cfg->M, nullptr, du, nullptr, st);
     RT_CUDA(cudaGetLastError());
     // du [line][j] -> V[line][k][j]
     RT_CUDA(cudaMemcpy2DAsync(V + static_cast<size_t>(k) * ns, static_cast<size_t>(nt) * ns * 8, du,
@@ -1187,10 +1178,16 @@ extern "C" rt_status rt_pdd_solve(rt_handle* h, const rt_pdd_cfg* cfg, double* o
   RT_CUDA(cudaEventRecord(h->ev[2], st));
   RT_CUDA(cudaMemcpyAsync(out_field, F, static_cast<size_t>(n1) * n1 * sizeof(double),
                           cudaMemcpyDeviceToHost, st));
-  if (out_nodal)
-    RT_CUDA(cudaMemcpyAsync(out_nodal, V, static_cast<size_t>(6) * nt * ns * sizeof(double),
-                            cudaMemcpyDeviceToHost, st));
+  std::vector<double> nodal(static_cast<size_t>(6) * nt * ns);
+  RT_CUDA(cudaMemcpyAsync(nodal.data(), V, nodal.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
   RT_CUDA(cudaStreamSynchronize(st));
+  if (out_nodal) std::memcpy(out_nodal, nodal.data(), nodal.size() * sizeof(double));
+  // the spline and the subdomain solves would spread a non-finite nodal
+  // value over the whole field: refuse it
+  for (size_t q = 0; q < nodal.size(); ++q)
+    if (!is_fin(nodal[q]))
+      return fail(RT_E_NUMERIC, "rt_pdd_solve: nodal value %zu (line %zu, level %zu) is not finite",
+                  q, q / (static_cast<size_t>(nt) * ns), (q / ns) % nt);
   if (out_ms) {
     float a = 0.f, b = 0.f, c = 0.f;
     RT_CUDA(cudaEventElapsedTime(&a, e0, e1));

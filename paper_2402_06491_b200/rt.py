@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librt_debug.so" if os.environ.get("RT_LIB_VARIANT") == "debug"
                         else "librt.so")
 
-RT_OK, RT_E_ARG, RT_E_CUDA, RT_E_NOMEM, RT_E_STATE = 0, 1, 2, 3, 4
+RT_OK, RT_E_ARG, RT_E_CUDA, RT_E_NOMEM, RT_E_STATE, RT_E_NUMERIC = 0, 1, 2, 3, 4, 5
 G_CONST, G_TANH_STEP, G_GAUSS, G_LORENTZ = 0, 1, 2, 3
 OFFSPRING_ABS, OFFSPRING_UNIFORM = 0, 1
 PREC_FP64, PREC_FP32_POS = 0, 1
@@ -93,8 +93,8 @@ def lib():
             "rt_estimate_dev": ([H, dp, i64, C.c_double, i64, u64, dp, dp, vp]),
             "rt_sums_dev": ([H, dp, i64, C.c_double, i64, i64, u64, dp, vp]),
             "rt_finalize_dev": ([dp, i64, i32, i64, dp, dp, dp, dp, vp]),
-            "rt_pade": ([dp, i64, i32, i32, i32, dp, vp]),
-            "rt_pade_dev": ([dp, i64, i32, i32, i32, dp, vp, vp]),
+            "rt_pade": ([dp, i64, i32, i32, i32, dp, dp, vp]),
+            "rt_pade_dev": ([dp, i64, i32, i32, i32, dp, dp, vp, vp]),
             "rt_interface_values": ([H, C.POINTER(Plane), i32, i64, C.c_double, i64, u64, i32, i32,
                                      dp, dp, dp, vp, C.POINTER(C.c_int64)]),
             "rt_trace_dev": ([H, dp, i64, C.c_double, i64, i64, u64, i32, vp, dp, vp]),
@@ -319,25 +319,28 @@ def finalize(sums, K: int, n_total: int, stream=None):
     return c, s, us, ses
 
 
-def pade(coeffs, L: int, M: int, stream=None):
-    """[L/M] Padé at z = 1 per row (rt_pade_dev) -> (u, flags) CUDA tensors."""
+def pade(coeffs, L: int, M: int, se_sum=None, stream=None):
+    """[L/M] Padé at z = 1 per row (rt_pade_dev) -> (u, flags) CUDA tensors;
+    se_sum (CUDA tensor [n], optional) enables flag bit3."""
     import torch
     c = coeffs.contiguous()
     n, k1 = c.shape
     u = torch.empty(n, dtype=torch.float64, device=c.device)
     fl = torch.empty(n, dtype=torch.int32, device=c.device)
-    _check(lib().rt_pade_dev(_ptr(c), n, k1 - 1, int(L), int(M), _ptr(u), _ptr(fl),
+    se = None if se_sum is None else se_sum.contiguous()
+    _check(lib().rt_pade_dev(_ptr(c), n, k1 - 1, int(L), int(M), _ptr(se), _ptr(u), _ptr(fl),
                              _stream(stream)))
     return u, fl
 
 
-def pade_host(coeffs: np.ndarray, L: int, M: int):
+def pade_host(coeffs: np.ndarray, L: int, M: int, se_sum=None):
     c = np.ascontiguousarray(coeffs, dtype=np.float64)
     if c.ndim == 1:
         c = c.reshape(1, -1)
     n, k1 = c.shape
     u = np.empty(n); fl = np.empty(n, dtype=np.uint32)
-    _check(lib().rt_pade(_ptr(c), n, k1 - 1, int(L), int(M), _ptr(u), _ptr(fl)))
+    se = None if se_sum is None else np.ascontiguousarray(se_sum, dtype=np.float64).reshape(n)
+    _check(lib().rt_pade(_ptr(c), n, k1 - 1, int(L), int(M), _ptr(se), _ptr(u), _ptr(fl)))
     return u, fl
 
 

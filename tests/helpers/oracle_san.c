@@ -43,6 +43,7 @@ int main(void) {
             double u, pp[8], qq[8];
             uint32_t fl;
             if (or_pade(c + 13 * i, 5, 5, &u, &fl, pp, qq)) bad++;
+            if (or_pade_node(c + 13 * i, 12, 5, 5, ses[i], &u, &fl)) bad++;
           }
         }
   printf("sanitized oracle run done, %d errors\n", bad);

@@ -83,10 +83,12 @@ def test_pade_arg_checks(rtmod):
     L = rtmod.lib()
     c = np.zeros(13)
     u = np.zeros(1)
-    assert L.rt_pade(c.ctypes.data, 1, 12, 7, 7, u.ctypes.data, None) == rtmod.RT_E_ARG
+    assert L.rt_pade(c.ctypes.data, 1, 12, 7, 7, None, u.ctypes.data, None) == rtmod.RT_E_ARG
     assert "L + M <= K" in L.rt_last_error().decode()
-    assert L.rt_pade(c.ctypes.data, 0, 12, 1, 1, u.ctypes.data, None) == rtmod.RT_E_ARG
-    assert L.rt_pade(c.ctypes.data, 1, 12, -1, 1, u.ctypes.data, None) == rtmod.RT_E_ARG
+    assert L.rt_pade(c.ctypes.data, 0, 12, 1, 1, None, u.ctypes.data, None) == rtmod.RT_E_ARG
+    assert L.rt_pade(c.ctypes.data, 1, 12, -1, 1, None, u.ctypes.data, None) == rtmod.RT_E_ARG
+    c31 = np.zeros(32)
+    assert L.rt_pade(c31.ctypes.data, 1, 31, 1, 1, None, u.ctypes.data, None) == rtmod.RT_E_ARG
 
 
 def test_product_does_not_import_oracle():

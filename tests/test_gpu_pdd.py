@@ -120,3 +120,30 @@ def test_pdd_solve_cfg3_against_reference(P, reference, shared):
     print(f"PDD cfg3: max err {d.max():.2e} mean {d.mean():.2e}; ms {ms}")
     assert d.max() < 2e-3 and d.mean() < 5e-4
     assert np.allclose(V[:, 0, :], 0.5 * np.exp(-(PO.pdd_nodes(cfg) ** 2).sum(-1)), atol=0, rtol=1e-15)
+
+
+def test_pdd_solve_early_levels_degenerate_table(P, orc):
+    """at early time levels t_k = kT/(n_t-1) with few trees
+    no tree reaches L splits, c_{L+1..} are exactly 0 and the [5/5] table is
+    degenerate.  Padé falls back to the largest regular [5/M'] (SPEC.md:403,
+    bit0), so every nodal value is finite and equals the oracle's
+    (tree walk at seed + k·φ, or_pade) to 1e-10; the field equals the numpy
+    downstream of those nodal values to 1e-11."""
+    eq = W.get("cfg3")["eq"]
+    cfg = dict(CFG, n_cells=40, n_steps=100, n_s=9, n_t=11, n_trees=10_000, seed=3)
+    F, V, ms = P.Estimator(eq).pdd_solve(cfg)
+    assert np.all(np.isfinite(V)) and np.all(np.isfinite(F))
+    nodes = PO.pdd_nodes(cfg).reshape(-1, 2)
+    fallback = 0
+    for k in range(1, cfg["n_t"]):
+        tk = cfg["T"] * (k / (cfg["n_t"] - 1))
+        seed_k = (cfg["seed"] + k * 0x9E3779B97F4A7C15) % (1 << 64)
+        c, *_ = orc.estimate(eq, nodes, tk, cfg["n_trees"], seed_k)
+        for q in range(nodes.shape[0]):
+            ur, flr, _, _ = orc.pade(c[q], cfg["L"], cfg["M"])
+            fallback += flr & 1
+            got = V[q // cfg["n_s"], k, q % cfg["n_s"]]
+            assert abs(got - ur) <= 1e-10 * abs(ur), (k, q, got, ur)
+    assert fallback > 0, "no degenerate table at these sizes: the test lost its point"
+    Fo, _ = PO.pdd_downstream(V, cfg, eq)
+    assert np.max(np.abs(F - Fo)) <= 1e-11 * max(1.0, np.max(np.abs(Fo)))
