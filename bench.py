@@ -37,37 +37,51 @@ import workloads as W  # noqa: E402
 # (MEASURED_PEAKS.json sm_max_mhz; /opt/skills/guides/B200_PROFILING.md).
 N_SM, FP64_LANES, F_MAX_MHZ = 148, 64, 1965.0
 
-# Algorithmic FP64 work: SURVEY.md §8(d)'s per-unit figure —
-# what the method itself must compute, costed with SURVEY's fixed table
-# (FP64 ops: log 20, exp 15, sincospi 20, sqrt 8, div 8, tanh 25;
-# fma/mul/add/compare 1) — times the units one launch processes (its event
-# counters).  Per particle: one exponential variate (1 log), ⌈d/2⌉ Box–Muller
-# pairs (each 1 log + 1 sqrt + 1 sincospi), 1 sqrt, d FMA + 1 sub + 1 compare
-# + 1 mul; per leaf: g (its argument, the transcendental or reciprocal, the
-# amplitude) + 1 mul; per split: 1 mul; per tree: 1 mul + 2 adds.  The
-# kernel's own cheaper math raises the achieved rate; it cannot inflate the
-# count.  (An earlier table costed each routine with CUDA libdevice's own
-# SASS — log 30, exp 18, sincospi 25, tanh 37 — and read 0.61 at cfg4.)
+# Algorithmic FP64 work: the FP64 operations the sampling
+# CONTRACT itself requires per unit, costed with SURVEY.md §8(d)'s fixed table
+# (FP64 ops: log 20, exp 15, sincospi 20 per angle, sqrt 8, div 8, tanh 25;
+# fma/mul/add/compare 1), times the units one launch processes (its event
+# counters).  The contract is DESIGN.md R29 for Strategy A: per particle ONE
+# Gamma(m+1) variate (m multiplies of the uniforms + 1 log), its split into
+# the clock and the radii' Exp(1) shares (m+1 multiplies, m subtractions),
+# S = e0/λ, the leaf test, 2D·h, τ - S, per radius 2 multiplies + 1 sqrt,
+# one angle per normal pair plus the third normal's (d = 3), d FMAs — not the
+# textbook draws SURVEY §8(d) listed (a log per exponential variate and per
+# Box–Muller radius), which the kernel does not perform.  Strategy B keeps
+# the textbook Box–Muller draws (R8).  Per leaf: g (its argument, the
+# transcendental or reciprocal, the amplitude) + 1 mul; per split: 1 mul;
+# per tree: 1 mul + 2 adds.  The FP32-position variant is credited only its
+# FP64 part (clock, weights, product, sums).  basis="survey" gives SURVEY
+# §8(d)'s original textbook count (reported beside it).
 SV = dict(log=20, exp=15, sqrt=8, div=8, tanh=25, sincospi=20)
 
 
-def algo_fp64_per_unit(eq: dict) -> dict:
+def algo_fp64_per_unit(eq: dict, basis: str = "contract") -> dict:
     d = eq["dim"]
     strat = eq.get("strategy", 0)
+    f32 = eq.get("precision", 0) == W.PREC_FP32_POS
     pairs = (d + 1) // 2
-    if strat == 2:                                         # Strategy B: ξ integer test,
-        clock = 2                                          # h = τS, τ_c = τ(1 - S)
+    if basis == "survey" or strat == 2:
+        clock = 2 if strat == 2 else SV["log"]             # B: h = τS, τ_c = τ(1 - S)
+        pos = (pairs * (SV["log"] + SV["sqrt"] + SV["sincospi"])
+               + SV["sqrt"] + d)                           # σ sqrt(h); y_k + (σ√h) ξ_k
+        per_particle = clock + pos + 3                     # τ - S, S > τ, 2D h
     else:
-        clock = SV["log"]                                  # S = -log(U)/λ
-    per_particle = (clock
-                    + pairs * (SV["log"] + SV["sqrt"] + SV["sincospi"])
-                    + SV["sqrt"]                           # σ sqrt(h)
-                    + d + 3)                               # y_k + (σ√h) ξ_k, τ - S, S > τ, 2D h
+        m = 1 if d <= 2 else 2                             # radii Exp(1) shares
+        gamma = m + SV["log"]                              # U1…U_{m+1}, -log
+        spacings = (m + 1) + m                             # G·spacing, spacing differences
+        clock = 4                                          # e0/λ, S > τ, 2D h, τ - S
+        radii = m * (2 + SV["sqrt"])                       # sqrt(2 e · 2Dh)
+        angles = (1 if d <= 2 else 2) * SV["sincospi"]
+        pos = radii + angles + d
+        per_particle = gamma + spacings + clock + (0 if f32 else pos)
     r2 = 2 * d - 1
     g = {W.G_CONST: 0,
          W.G_TANH_STEP: 1 + SV["tanh"] + 2,                # x/s, tanh, amp (1 + ·)/2
          W.G_GAUSS: r2 + 1 + SV["exp"] + 1,                # |x|², /s², exp, amp
          W.G_LORENTZ: r2 + 1 + 1 + SV["div"] + 1}[eq["init_kind"]]   # |x|², /s², 1 +, 1/·, amp
+    if f32 and basis != "survey":
+        g = 0                                              # g in single precision
     split = 1                                              # Π *= w_k
     if strat == 1:
         split += SV["exp"] + 2                             # e^{(k-1)λτ_c}
@@ -81,14 +95,14 @@ def algo_fp64_per_unit(eq: dict) -> dict:
                 tree=3 + (1 if strat == 1 else 0))         # ΣC += C, ΣC² += C·C (× e^{λt})
 
 
-def algo_fp64_ops(eq: dict, stats: dict, n_points: int = 1) -> float:
+def algo_fp64_ops(eq: dict, stats: dict, n_points: int = 1, basis: str = "contract") -> float:
     """Algorithmic FP64 lane-ops of one launch from its event counters.
 
     Shared trees (f4): the statistics count per (node, tree), but the method
     walks each tree once for all n_points nodes — particles and splits are
     credited once per tree; the g evaluations (leaves) and the per-tree
     accumulation happen per node."""
-    u = algo_fp64_per_unit(eq)
+    u = algo_fp64_per_unit(eq, basis)
     walk = 1.0 / n_points if eq.get("shared") else 1.0
     return (stats["particles"] * walk * u["particle"] + stats["leaves"] * u["leaf"] +
             stats["splits"] * walk * u["split"] + stats["trees"] * u["tree"])
@@ -402,6 +416,7 @@ def main():
     value = trees_all / (tot_ms / 1e3)
     leaves_all = st_one["leaves"] * ws * args.steps
     ops = algo_fp64_ops(eq, st_one, n)
+    ops_survey = algo_fp64_ops(eq, st_one, n, basis="survey")
     peak = N_SM * FP64_LANES * F_MAX_MHZ * 1e6 / 1e12       # T lane-ops/s
     achieved = ops / (walk_avg / 1e3) / 1e12
     clocks = clk.summary()
@@ -410,13 +425,18 @@ def main():
         k0 = P.rt.fp64_peak()["lane_ops_per_s"] / 1e12
     except Exception:   # noqa: BLE001 — diagnostic only
         k0 = None
-    # DRAM traffic of the tree-walk launch from the committed ncu capture of
-    # this same command (profiles/r1/traffic_<workload>.json), else null
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "r1", f"traffic_{cfg['name']}.json")
-    if os.path.exists(tf) and not args.trees:
-        tj = json.load(open(tf))
-        traffic = tj["dram_bytes_read"] + tj["dram_bytes_write"]
+    # DRAM traffic and the hardware FP64-pipe share of the tree-walk launch
+    # from the committed ncu captures of this same command
+    # (profiles/r2/traffic_<workload>.json, the latest round first), else null
+    traffic, hw = None, {}
+    for rnd in ("r2", "r1"):
+        tf = os.path.join(ROOT, "profiles", rnd, f"traffic_{cfg['name']}.json")
+        if os.path.exists(tf) and not args.trees:
+            tj = json.load(open(tf))
+            traffic = tj["dram_bytes_read"] + tj["dram_bytes_write"]
+            hw = {k: tj[k] for k in ("fp64_pipe_pct", "issue_active_pct", "inst_per_iteration",
+                                     "source") if k in tj}
+            break
 
     # ---- end to end through the public host API (rt_interface_values) -----
     e2e = None
@@ -507,6 +527,9 @@ def main():
                      "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read + write)",
                      "launch_ms": walk_avg,
                      "algorithmic_fp64_ops_per_launch": ops,
+                     "basis": "DESIGN.md R29 contract units (one log per particle), SURVEY 8(d) cost table",
+                     "frac_survey_textbook_table": ops_survey / (walk_avg / 1e3) / 1e12 / peak,
+                     "ncu_hardware": hw or None,
                      "peak_basis": "148 SM x 64 FP64 lanes/clk x 1965 MHz (B200_PROFILING.md nominal; MEASURED_PEAKS.json has no FP64 entry)",
                      "frac_at_measured_clock": (achieved / (N_SM * FP64_LANES * clocks["sm_mhz"] * 1e6 / 1e12)
                                                 if clocks.get("sm_mhz") else None),

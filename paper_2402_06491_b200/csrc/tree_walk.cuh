@@ -218,6 +218,19 @@ __device__ __forceinline__ void red_add(double* p, double v) {
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
+// The same with an L2 eviction-priority hint: the lane-private bin sums
+// (65 MB at cfg4) are the kernel's only re-used global data, so they are
+// kept resident (evict_last) while the once-written task partials stream
+// past them (evict_first), instead of being written back to DRAM.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void red_add_keep(double* p, double v, uint64_t pol) {
+  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 // F32 = the FP32-position / FP64-accumulate variant (cfg5, BASELINE.json
 // configs[4]): the clock S, the leaf test, horizons, weights, the tree
 // product and all sums stay FP64 (tree structure identical to the FP64
@@ -327,7 +340,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 
   // ---- lane state ----------------------------------------------------------
   bool active = false;
-  uint32_t ti = 0, tj = 0;
+  uint32_t tj = 0;   // (the node is the task's: warp-uniform iss_node)
   PT y[DIM];
 #pragma unroll
   for (int k = 0; k < DIM; ++k) y[k] = PT(0);
@@ -338,7 +351,6 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   int c_part = 0, c_leaf = 0;          // particles / leaves since the last task close
 
   auto start_tree = [&](uint32_t j) {  // a fresh tree j of the current task
-    ti = iss_node;
     tj = j;
 #pragma unroll
     for (int k = 0; k < DIM; ++k) y[k] = SH ? PT(0) : static_cast<PT>(ws->iss_y[k]);   // SH: δ = 0
@@ -370,7 +382,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
         if (lane == 0) {
           double* o = P.partials + (static_cast<int64_t>(task) * P.nb + b) * 3;
           const bool prb = b == P.K + 1;           // pruned bin: count only
-          o[0] = prb ? 0.0 : v1; o[1] = prb ? 0.0 : v2; o[2] = v3;
+          __stcs(o, prb ? 0.0 : v1); __stcs(o + 1, prb ? 0.0 : v2); __stcs(o + 2, v3);
         }
       }
     }
@@ -422,6 +434,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 
   if (lane == 0) ws->gtop = ws->gfree = 0;
   __syncthreads();
+  const uint64_t pol = l2_evict_last_policy();   // (warp-uniform: a uniform register)
   next_task();
   if (!stream_end) {
     const uint32_t take = min(iss_end - iss_next, 32u);
@@ -437,7 +450,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     // ---------------- one particle per lane (converged) ----------------------
     const uint32_t c2 = static_cast<uint32_t>(label);
     const uint32_t c3 = static_cast<uint32_t>(label >> 32);
-    const uint32_t c1 = SH ? 0u : ti;           // shared trees: no node in the counter
+    const uint32_t c1 = SH ? 0u : iss_node;     // the task's node (shared trees: none)
     const uint4 r0 = philox4x32_10(tj, c1, c2, c3, P.rk);
     const uint4 r1 = philox4x32_10(tj, c1, c2, c3 | (1u << 24), P.rk);
     bool leaf;
@@ -710,7 +723,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
         TreeRec r;
         r.ne = ne; r.leaves = leaves; r.particles = parts; r.pruned = pruned ? 1 : 0;
         r.C = pruned ? 0.0 : Pi;
-        P.recs[static_cast<int64_t>(ti) * P.n_rec + (rel >> P.rec_shift)] = r;
+        P.recs[static_cast<int64_t>(iss_node) * P.n_rec + (rel >> P.rec_shift)] = r;
       }
     }
 
@@ -755,9 +768,9 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
         if (done) {                                 // bin ne (= K+1, the pruned bin, iff pruned)
           RT_CHECK(ne >= 0 && ne < P.nb);
           double* a = lacc() + ne * 96;
-          red_add(a, Pi);
-          red_add(a + 32, Pi * Pi);
-          red_add(a + 64, 1.0);
+          red_add_keep(a, Pi, pol);
+          red_add_keep(a + 32, Pi * Pi, pol);
+          red_add_keep(a + 64, 1.0, pol);
         }
       }
       left -= nfin;

@@ -11,17 +11,28 @@ import workloads as W  # noqa: E402
 
 
 def test_cost_model_per_unit_counts():
-    """Per-unit costs are SURVEY.md §8(d)'s list: one exponential variate,
-    ⌈d/2⌉ Box–Muller pairs, one sqrt, d + 3 plain ops per particle."""
+    """Contract units (R29): per particle ONE Gamma(m+1)
+    variate (m multiplies + 1 log), its m+1 shares (m+1 multiplies, m
+    subtractions), 4 clock ops, per radius 2 multiplies + 1 sqrt, one angle
+    per normal pair (+ the third normal's), d FMAs.  basis="survey" is SURVEY
+    §8(d)'s textbook list: one exponential variate, ⌈d/2⌉ Box–Muller pairs,
+    one sqrt, d + 3 plain ops."""
     u1 = bench.algo_fp64_per_unit(W.get("cfg2")["eq"])
     u3 = bench.algo_fp64_per_unit(W.get("cfg4")["eq"])
-    assert u1["particle"] == 20 + 1 * (20 + 8 + 20) + 8 + 1 + 3 == 80
-    assert u3["particle"] == 20 + 2 * (20 + 8 + 20) + 8 + 3 + 3 == 130
+    assert u1["particle"] == (1 + 20) + (2 + 1) + 4 + 1 * (2 + 8) + 20 + 1 == 59
+    assert u3["particle"] == (2 + 20) + (3 + 2) + 4 + 2 * (2 + 8) + 2 * 20 + 3 == 94
+    s1 = bench.algo_fp64_per_unit(W.get("cfg2")["eq"], basis="survey")
+    s3 = bench.algo_fp64_per_unit(W.get("cfg4")["eq"], basis="survey")
+    assert s1["particle"] == 20 + 1 * (20 + 8 + 20) + 8 + 1 + 3 == 80
+    assert s3["particle"] == 20 + 2 * (20 + 8 + 20) + 8 + 3 + 3 == 130
     assert u3["tree"] == 3 and u1["split"] == 1
     # Lorentzian g (cfg4): |x|² (2d-1) + /s² + 1 + reciprocal (div 8) + amp, then Π *= g
-    assert u3["leaf"] == 5 + 1 + 1 + 8 + 1 + 1
+    assert u3["leaf"] == s3["leaf"] == 5 + 1 + 1 + 8 + 1 + 1
     # Gaussian g (cfg2, d = 1): x² + /s² + exp 15 + amp, then Π *= g
     assert u1["leaf"] == 1 + 1 + 15 + 1 + 1
+    # FP32 positions: only the FP64 part (clock, weights, product, sums)
+    u32 = bench.algo_fp64_per_unit(dict(W.get("cfg2")["eq"], precision=W.PREC_FP32_POS))
+    assert u32["particle"] == (1 + 20) + (2 + 1) + 4 and u32["leaf"] == 1
 
 
 def test_shared_trees_credit_the_walk_once():
@@ -46,7 +57,7 @@ def test_cost_model_strategies():
     base = W.get("ex1A")["eq"]
     ua = bench.algo_fp64_per_unit(base)                       # shift
     ub = bench.algo_fp64_per_unit(W.get("ex1B")["eq"])        # Strategy B
-    up = bench.algo_fp64_per_unit(dict(base, strategy=0))     # potential
+    up = bench.algo_fp64_per_unit(dict(base, strategy=0), basis="survey")   # potential
     assert up["particle"] - ub["particle"] == 20 - 2
     assert ua["split"] == up["split"] + 15 + 2 and ua["tree"] == up["tree"] + 1
     assert ub["split"] == up["split"] + 1 and ub["leaf"] == up["leaf"] + 1
