@@ -256,15 +256,15 @@ extern "C" rt_status rt_set_pool(rt_handle* h, int32_t pool_entries) {
 // tree-walk launch (rows a3–a7)
 using KernelFn = void (*)(WalkParams);
 
-template <int DIM, int GK, bool REC, bool F32, bool SB, bool SH = false>
+template <int DIM, int GK, bool REC, bool F32, bool SB, bool SH = false, bool GEN = true>
 static KernelFn pick_kernel() {
-  return rtk::tree_walk_kernel<DIM, GK, REC, F32, SB, SH>;
+  return rtk::tree_walk_kernel<DIM, GK, REC, F32, SB, SH, GEN>;
 }
 
 // The kernel for (dim, g, rec) and the production (rec = false) kernel whose
 // occupancy fixes the launch geometry for both.
-static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, bool sb, bool sh, KernelFn* prod,
-                           int* smem, int* pool_cap) {
+static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, bool sb, bool sh, bool gen,
+                           KernelFn* prod, int* smem, int* pool_cap) {
 #define RT_K(D, G)                                                              \
   if (dim == D && gk == G) {                                                    \
     *smem = rtk::smem_bytes<D>();                                               \
@@ -281,9 +281,17 @@ static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, bool sb, bool sh
       *prod = pick_kernel<D, G, false, false, true>();                          \
       return rec ? pick_kernel<D, G, true, false, true>() : *prod;              \
     }                                                                           \
+    if (f32 && !gen) {                                                          \
+      *prod = pick_kernel<D, G, false, true, false, false, false>();            \
+      return rec ? pick_kernel<D, G, true, true, false, false, false>() : *prod; \
+    }                                                                           \
     if (f32) {                                                                  \
       *prod = pick_kernel<D, G, false, true, false>();                          \
       return rec ? pick_kernel<D, G, true, true, false>() : *prod;              \
+    }                                                                           \
+    if (!gen) {                                                                 \
+      *prod = pick_kernel<D, G, false, false, false, false, false>();           \
+      return rec ? pick_kernel<D, G, true, false, false, false, false>() : *prod; \
     }                                                                           \
     *prod = pick_kernel<D, G, false, false, false>();                           \
     return rec ? pick_kernel<D, G, true, false, false>() : *prod;               \
@@ -614,8 +622,12 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   int smem = 0, pool_cap = 0;
   KernelFn prod = nullptr;
   const bool sh = p.shared != 0;
+  bool var = false;
+  for (int k = 0; k <= 8; ++k) var = var || p.coef_kind[k] != RT_COEF_CONST;
+  // the general kernel only where f2/f3 weight factors or > 3 offspring kinds need it
+  const bool gen = p.strategy != RT_STRATEGY_POTENTIAL || var || nz.n_support > 3;
   KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, p.precision == RT_PREC_FP32_POS,
-                           p.strategy == RT_STRATEGY_B, sh, &prod, &smem, &pool_cap);
+                           p.strategy == RT_STRATEGY_B, sh, gen, &prod, &smem, &pool_cap);
   if (!fn) return fail(RT_E_ARG, "no kernel for dim=%d init_kind=%d", p.dim, p.init_kind);
   if (smem > 48 * 1024) {
     RT_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

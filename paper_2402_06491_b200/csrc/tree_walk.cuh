@@ -243,7 +243,10 @@ __device__ __forceinline__ void red_add_keep(double* p, double v, uint64_t pol) 
 // range; lanes walk trees carrying the displacement δ from the root and write
 // each tree's summary (TreeSum) and leaf displacements; phase 2
 // (shared_eval.cuh) evaluates all nodes.  Constant coefficients only.
-template <int DIM, int GK, bool REC, bool F32, bool SB, bool SH>
+// GEN = false: the common equations — no f2/f3 weight factors (wmode = 0)
+// and at most three offspring kinds — without the warp-uniform tests for the
+// rest (the same arithmetic; chosen by the launcher).
+template <int DIM, int GK, bool REC, bool F32, bool SB, bool SH, bool GEN = true>
 __global__ void __launch_bounds__(kThreads, MinCtas<DIM, REC>::v)
 tree_walk_kernel(const __grid_constant__ WalkParams P) {
   using PT = typename std::conditional<F32, float, double>::type;   // position type
@@ -556,7 +559,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     int s = 0;
     inc_if(c32 > P.thr[0], s);
     inc_if(c32 > P.thr[1], s);
-    if (P.n_support > 3) {                      // warp-uniform
+    if (GEN && P.n_support > 3) {               // warp-uniform
       inc_if(c32 > P.thr[2], s);
       inc_if(c32 > P.thr[3], s);
       if (P.n_support > 5) {                    // warp-uniform, rare
@@ -570,7 +573,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const int k = ktab[s];
     double wk = wtab[s];
     if constexpr (SB) wk *= tau;                // η(τ) = τ
-    if (P.wmode != 0) {                         // warp-uniform: f2/f3 weight factors
+    if (GEN && P.wmode != 0) {                  // warp-uniform: f2/f3 weight factors
       double f = 1.0;
       if ((P.var_s >> s) & 1u) {                // c_k(y, τ_c) = b_k e^{-y_a²/s²}/(τ_c + t0)
         double ya = static_cast<double>(y[0]);   // (no dynamic register indexing)
