@@ -781,7 +781,9 @@ extern "C" rt_status rt_get_stats(const rt_handle* hc, rt_stats* out) {
   RT_CUDA(cudaMemcpy(v, h->stats.p, sizeof(v), cudaMemcpyDeviceToHost));
   out->trees = static_cast<int64_t>(v[0]);
   out->pruned = static_cast<int64_t>(v[1]);
-  out->particles = static_cast<int64_t>(v[2]);
+  // every processed particle reaches its horizon (a leaf) or splits — the
+  // aborting split of a pruned tree included (the kernel counts no particles)
+  out->particles = static_cast<int64_t>(v[3]) + static_cast<int64_t>(v[4]);
   out->leaves = static_cast<int64_t>(v[3]);
   out->splits = static_cast<int64_t>(v[4]);
   float ms = 0.f;

@@ -351,13 +351,13 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   uint64_t label = 1;
   int ne = 0, top = -1;                // top: the lane's top stack entry (-1: empty)
   int leaves = 0, parts = 0;           // per-tree counts (trace variant only)
-  int c_part = 0, c_leaf = 0;          // particles / leaves since the last task close
+  int c_leaf = 0;                      // leaves since the last task close
 
   auto start_tree = [&](uint32_t j) {  // a fresh tree j of the current task
     tj = j;
 #pragma unroll
     for (int k = 0; k < DIM; ++k) y[k] = SH ? PT(0) : static_cast<PT>(ws->iss_y[k]);   // SH: δ = 0
-    tau = P.t; label = 1; Pi = P.root; ne = 0; top = -1;
+    tau = P.t; label = 1; Pi = GEN ? P.root : 1.0; ne = 0; top = -1;   // (GEN = false: no shift, root factor 1)
     if constexpr (REC || SH) { leaves = 0; parts = 0; }
     active = true;
   };
@@ -390,19 +390,14 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       }
     }
     // (shared trees: every node sees each walked particle and leaf)
+    // (particles = leaves + splits: every processed particle either reaches
+    // its horizon or splits — the aborting split included — so the host
+    // derives them; splits come exactly from the bin counts)
     const unsigned long long scale = SH ? static_cast<unsigned long long>(P.n_points) : 1ull;
-    unsigned long long v0 = static_cast<unsigned long long>(c_part) * scale,
-                       v1 = static_cast<unsigned long long>(c_leaf) * scale;
+    unsigned long long v1 = static_cast<unsigned long long>(c_leaf) * scale;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      v0 += __shfl_xor_sync(0xffffffffu, v0, o);
-      v1 += __shfl_xor_sync(0xffffffffu, v1, o);
-    }
-    if (lane == 0) {
-      atomicAdd(P.stats + 2, v0);
-      atomicAdd(P.stats + 3, v1);
-    }
-    c_part = 0;
+    for (int o = 16; o > 0; o >>= 1) v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+    if (lane == 0) atomicAdd(P.stats + 3, v1);
     c_leaf = 0;
     next_task();
     if (!stream_end) {
@@ -603,7 +598,6 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     // discarded at task close)
     const double fac = leaf ? (SB ? gl * P.inv_q : gl) : wk;
     Pi *= fac;                                   // (an idle lane's product is never recorded)
-    inc_if(active, c_part);
     inc_if(active && leaf, c_leaf);
     if constexpr (REC || SH) {
       inc_if(active, parts);
@@ -801,7 +795,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     P.wtime[4 * gwarp + 3] = 0;   // (iteration count: not recorded)
   }
   // (trees, pruned trees and splits follow exactly from the bin counts and are
-  // added by the task-reduction kernel; every task close folded c_part/c_leaf)
+  // added by the task-reduction kernel; every task close folded c_leaf)
 }
 
 }  // namespace rtk
