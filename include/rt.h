@@ -119,7 +119,7 @@ typedef struct {
 typedef struct {
   int64_t trees;        /* trees sampled (kept + pruned)                 */
   int64_t pruned;       /* trees with Ne > K                             */
-  int64_t particles;    /* particle lifetimes simulated                  */
+  int64_t particles;    /* particle lifetimes simulated (= leaves + splits) */
   int64_t leaves;       /* g evaluations                                 */
   int64_t splits;       /* splitting events (incl. the aborting one)     */
   double  kernel_ms;    /* tree-walk kernel time of the last estimate    */
@@ -165,8 +165,10 @@ rt_status rt_destroy(rt_handle* h);
  * per node, and copies back the per-order coefficients c_n = ΣC_n / N and
  * standard errors se_n = sqrt(max(0, ΣC_n²/N − c_n²)/(N−1)), n = 0..K, where
  * N = n_trees counts pruned trees (R4, R11).
- * RT_E_ARG on: null pointers, n_points < 1, t <= 0 or non-finite, n_trees < 2
- * or > 2^32, non-finite points.  Times the copies inside rt_stats.total_ms.
+ * RT_E_ARG on: null pointers, n_points < 1 or >= 2^31, t <= 0 or non-finite,
+ * n_trees < 2 or >= 2^31 (per call; larger counts are split over calls with
+ * rt_sums_dev's tree_offset), non-finite points.  Times the copies inside
+ * rt_stats.total_ms.
  * Tree j of node i draws Philox4x32-10 blocks keyed by (seed; j, i, particle
  * label, call), mapped to its clock and Gaussian increments as DESIGN.md R29
  * (Strategy A: one Gamma variate split into the clock and the Box-Muller

@@ -56,8 +56,8 @@ def main():
     tests = os.path.join(OUT, f"gpu_tests_{tag}.log")
     if os.path.exists(tests):
         md += ["`pytest -m gpu`: " + " ".join(open(tests).read().strip().splitlines()[-2:]), ""]
-    md += ["## Bench lines (`python bench.py`; cfg2 with `--config cfg2`)", ""]
-    for cfg in ("cfg4", "cfg2"):
+    md += ["## Bench lines (`python bench.py`; the others with `--config <cfg>`)", ""]
+    for cfg in ("cfg4", "cfg1", "cfg2", "cfg3"):
         b = bench_line(os.path.join(OUT, f"bench_{cfg}_{tag}.log"))
         if not b:
             continue
@@ -65,7 +65,10 @@ def main():
         md.append(f"- **{cfg}**: {b['value']:.4g} trees/s, {b['leaf_evals_per_s']:.4g} leaf-evals/s, "
                   f"{b['ms_per_step']:.2f} ms/step; tree-walk launch {rf['launch_ms']:.2f} ms; "
                   f"roofline ({rf['bound']}) achieved {rf['achieved']:.3f} of {rf['peak']:.3f} {rf['unit']} "
-                  f"= **{rf['frac']:.3f}**; clocks {b['clocks']}; e2e {b['e2e']['value']:.4g} trees/s"
+                  f"= **{rf['frac']:.3f}**"
+                  + (f" (SURVEY textbook table {rf['frac_survey_textbook_table']:.3f})"
+                     if "frac_survey_textbook_table" in rf else "")
+                  + f"; clocks {b['clocks']}; e2e {b['e2e']['value']:.4g} trees/s"
                   + (f"; oracle {b['cpu_baseline']['value']:.4g} trees/s on {b['cpu_baseline']['cores']} core"
                      if b.get("cpu_baseline") else ""))
         shutil.copy(os.path.join(OUT, f"bench_{cfg}_{tag}.log"), dst)
@@ -81,9 +84,18 @@ def main():
             md.append(f"| `{k}` | {n[k]} | {v / 1e6:.3f} | {v / T * 100:.2f} % | {v / n[k] / 1e6:.3f} |")
         md.append("")
         shutil.copy(lc, dst)
-    rep = os.path.join(OUT, f"prof_tw_{tag}.ncu-rep")
-    if os.path.exists(rep):
-        md += ["## ncu --set full, tree-walk kernel (cfg4 equation, 1024 nodes x 2e5 trees)", "", "```",
+    tc = os.path.join(OUT, f"traffic_cfg4_{tag}.csv")
+    if os.path.exists(tc):
+        md += ["## ncu hardware counters, one full-size cfg4 tree-walk launch", "", "```",
+               run([sys.executable, "tools/traffic_json.py", tc, "cfg4", tag]).strip(), "```", ""]
+        shutil.copy(tc, dst)
+    for name, what in ((f"prof_tw_{tag}", "cfg4 equation, 1024 nodes x 2e5 trees"),
+                       (f"prof_tw_cfg4_{tag}", "cfg4 equation, 1024 nodes x 2e5 trees"),
+                       (f"prof_tw_cfg2_{tag}", "cfg2, 64 nodes x 1e6 trees")):
+        rep = os.path.join(OUT, name + ".ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        md += [f"## ncu --set full, tree-walk kernel ({what})", "", "```",
                run([sys.executable, "tools/ncu_summary.py", rep]).strip(), "```", "",
                "Per-iteration instruction budget (runs of equal execution count):", "", "```",
                run([sys.executable, "tools/ncu_blocks.py", rep]).strip(), "```", ""]
