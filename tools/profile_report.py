@@ -99,7 +99,9 @@ def main():
                run([sys.executable, "tools/ncu_summary.py", rep]).strip(), "```", "",
                "Per-iteration instruction budget (runs of equal execution count):", "", "```",
                run([sys.executable, "tools/ncu_blocks.py", rep]).strip(), "```", ""]
-        shutil.copy(rep, dst)
+        if "cfg2" not in name:   # the report (30 MB with sources) travels xz-compressed
+            subprocess.run(["xz", "-9", "-T8", "-c", rep], stdout=open(
+                os.path.join(dst, name + ".ncu-rep.xz"), "wb"), check=True)
     path = os.path.join(dst, f"{tag}.md")
     with open(path, "w") as f:
         f.write("\n".join(md) + "\n")
