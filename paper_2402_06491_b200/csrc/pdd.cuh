@@ -3,9 +3,9 @@
 // into Dirichlet data and four fully decoupled subdomain solves
 // ("Interpolation" and "Local solver", 1007-1012).
 //
-//   pdd_spline_kernel: one thread per (line, grid node s_i): the tensor-product
-//     not-a-knot cubic spline in (s, t) of that line's nodal table
-//     (PAPER.md:939-942), evaluated at s_i for every time step t_n.
+//   pdd_spline_s_kernel + pdd_spline_t_kernel: the tensor-product not-a-knot
+//     cubic spline in (s, t) of each line's nodal table,
+//     evaluated at every grid node s_i for every time step t_n.
 //   pdd_adi_kernel: one CTA per subdomain (the paper's "each subdomain ...
 //     assigned to different processors" — here an SM each), the whole time
 //     march in shared memory: Strang splitting with RK4 half reactions and a
@@ -30,34 +30,50 @@ constexpr int kPddMaxNodes = 64;    // ns, nt <= 64
 // (third derivative continuous at x_1, x_{n-2}) the first and last interior
 // C² equations reduce to 6 M_1 = r_1 and 6 M_{n-2} = r_{n-2}; the rest is the
 // tridiagonal (1, 4, 1) system, r_i = 6 (y_{i+1} - 2 y_i + y_{i-1}) / h².
-__device__ inline void nak_m(const double* y, int n, double h, double* M) {
-  double cp[kPddMaxNodes], dp[kPddMaxNodes];
+// y and M are strided (element i at y[i*ys], M[i*ms]); M doubles as the
+// Thomas sweep's d' storage, and the factors c'_i (the same for every system
+// of size n) come precomputed in cp — no local arrays.
+__device__ inline void nak_m(const double* y, int ys, int n, double h, double* M, int ms,
+                             const double* cp) {
   const double s = 6.0 / (h * h);
-  M[1] = (y[2] - 2.0 * y[1] + y[0]) * s / 6.0;
-  M[n - 2] = (y[n - 1] - 2.0 * y[n - 2] + y[n - 3]) * s / 6.0;
-  // interior unknowns M_2..M_{n-3} (Thomas)
+  const double m1 = (y[2 * ys] - 2.0 * y[ys] + y[0]) * s / 6.0;
+  const double mn = (y[(n - 1) * ys] - 2.0 * y[(n - 2) * ys] + y[(n - 3) * ys]) * s / 6.0;
+  // interior unknowns M_2..M_{n-3} (Thomas; d'_i stored in M_i)
   const int a = 2, b = n - 3;
+  double prev = 0.0;
   for (int i = a; i <= b; ++i) {
-    double r = (y[i + 1] - 2.0 * y[i] + y[i - 1]) * s;
-    if (i == a) r -= M[1];
-    if (i == b) r -= M[n - 2];
+    double r = (y[(i + 1) * ys] - 2.0 * y[i * ys] + y[(i - 1) * ys]) * s;
+    if (i == a) r -= m1;
+    if (i == b) r -= mn;
     const double den = (i == a) ? 4.0 : 4.0 - cp[i - 1];
-    cp[i] = 1.0 / den;
-    dp[i] = (i == a) ? r / den : (r - dp[i - 1]) / den;
+    prev = (i == a) ? r / den : (r - prev) / den;
+    M[i * ms] = prev;
   }
-  for (int i = b; i >= a; --i) M[i] = (i == b) ? dp[i] : dp[i] - cp[i] * M[i + 1];
-  M[0] = 2.0 * M[1] - M[2];
-  M[n - 1] = 2.0 * M[n - 2] - M[n - 3];
+  double nxt = 0.0;
+  for (int i = b; i >= a; --i) {
+    nxt = (i == b) ? M[i * ms] : M[i * ms] - cp[i] * nxt;
+    M[i * ms] = nxt;
+  }
+  M[ms] = m1;
+  M[(n - 2) * ms] = mn;
+  M[0] = 2.0 * m1 - M[2 * ms];
+  M[(n - 1) * ms] = 2.0 * mn - M[(n - 3) * ms];
 }
 
-__device__ inline double nak_at(const double* y, const double* M, int n, double x0, double h,
-                                double x) {
+// c'_i = 1/den_i of nak_m's Thomas sweep for a system of n nodes (i = 2..n-3)
+__device__ inline void nak_factors(int n, double* cp) {
+  for (int i = 2; i <= n - 3; ++i) cp[i] = 1.0 / ((i == 2) ? 4.0 : 4.0 - cp[i - 1]);
+}
+
+__device__ inline double nak_at(const double* y, int ys, const double* M, int ms, int n, double x0,
+                                double h, double x) {
   int j = static_cast<int>(floor((x - x0) / h));
   j = j < 0 ? 0 : (j > n - 2 ? n - 2 : j);
   const double a = x0 + j * h, b = a + h;
-  return M[j] * (b - x) * (b - x) * (b - x) / (6.0 * h) +
-         M[j + 1] * (x - a) * (x - a) * (x - a) / (6.0 * h) +
-         (y[j] / h - M[j] * h / 6.0) * (b - x) + (y[j + 1] / h - M[j + 1] * h / 6.0) * (x - a);
+  const double Mj = M[j * ms], Mj1 = M[(j + 1) * ms], yj = y[j * ys], yj1 = y[(j + 1) * ys];
+  return Mj * (b - x) * (b - x) * (b - x) / (6.0 * h) +
+         Mj1 * (x - a) * (x - a) * (x - a) / (6.0 * h) +
+         (yj / h - Mj * h / 6.0) * (b - x) + (yj1 / h - Mj1 * h / 6.0) * (x - a);
 }
 
 struct PddGeom {
@@ -65,25 +81,45 @@ struct PddGeom {
   int n, m, ns, nt, n_steps;
 };
 
-// W[line][step][i] from V[line][k][j]; one thread per (line, i).
-__global__ void pdd_spline_kernel(const double* __restrict__ V, double* __restrict__ W,
-                                  PddGeom G, int n_lines) {
+// Interpolation, two passes with no local memory:
+// pdd_spline_s_kernel: one thread per (line, time level k): the spline in s
+//   of V[line][k][·] — its second derivatives Ms[line][k][·];
+// pdd_spline_t_kernel: one thread per (line, grid node i): A[k] = that
+//   spline at s = x_i for every level, the spline in t through A (second
+//   derivatives in At), evaluated at every time step into W[line][step][i].
+//   A and At are [line][k][i] (coalesced across the threads i).
+__global__ void pdd_spline_s_kernel(const double* __restrict__ V, double* __restrict__ Ms, PddGeom G,
+                                    int n_lines) {
+  __shared__ double cp[kPddMaxNodes];
+  if (threadIdx.x == 0) nak_factors(G.ns, cp);
+  __syncthreads();
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= n_lines * (G.n + 1)) return;
-  const int line = q / (G.n + 1), i = q - line * (G.n + 1);
+  if (q >= n_lines * G.nt) return;
+  const double hs = (G.hi - G.lo) / (G.ns - 1);
+  nak_m(V + static_cast<int64_t>(q) * G.ns, 1, G.ns, hs, Ms + static_cast<int64_t>(q) * G.ns, 1, cp);
+}
+
+__global__ void pdd_spline_t_kernel(const double* __restrict__ V, const double* __restrict__ Ms,
+                                    double* __restrict__ A, double* __restrict__ At,
+                                    double* __restrict__ W, PddGeom G, int n_lines) {
+  __shared__ double cp[kPddMaxNodes];
+  if (threadIdx.x == 0) nak_factors(G.nt, cp);
+  __syncthreads();
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n1 = G.n + 1;
+  if (q >= n_lines * n1) return;
+  const int line = q / n1, i = q - line * n1;
   const double x = G.lo + i * G.h;
   const double hs = (G.hi - G.lo) / (G.ns - 1), ht = G.T / (G.nt - 1);
-  double row[kPddMaxNodes], M[kPddMaxNodes], A[kPddMaxNodes], Ma[kPddMaxNodes];
-  const double* Vl = V + static_cast<int64_t>(line) * G.nt * G.ns;
-  for (int k = 0; k < G.nt; ++k) {          // splines in s at every time node
-    for (int j = 0; j < G.ns; ++j) row[j] = Vl[k * G.ns + j];
-    nak_m(row, G.ns, hs, M);
-    A[k] = nak_at(row, M, G.ns, G.lo, hs, x);
-  }
-  nak_m(A, G.nt, ht, Ma);                    // then the spline in t at s = x_i
-  double* Wl = W + static_cast<int64_t>(line) * (G.n_steps + 1) * (G.n + 1) + i;
+  const int64_t vb = static_cast<int64_t>(line) * G.nt * G.ns;
+  double* Al = A + static_cast<int64_t>(line) * G.nt * n1 + i;       // A[line][k][i]
+  double* Atl = At + static_cast<int64_t>(line) * G.nt * n1 + i;
+  for (int k = 0; k < G.nt; ++k)              // splines in s at every time node
+    Al[static_cast<int64_t>(k) * n1] = nak_at(V + vb + k * G.ns, 1, Ms + vb + k * G.ns, 1, G.ns, G.lo, hs, x);
+  nak_m(Al, n1, G.nt, ht, Atl, n1, cp);      // then the spline in t at s = x_i
+  double* Wl = W + static_cast<int64_t>(line) * (G.n_steps + 1) * n1 + i;
   for (int st = 0; st <= G.n_steps; ++st)
-    Wl[static_cast<int64_t>(st) * (G.n + 1)] = nak_at(A, Ma, G.nt, 0.0, ht, st * G.dt);
+    Wl[static_cast<int64_t>(st) * n1] = nak_at(Al, n1, Atl, n1, G.nt, 0.0, ht, st * G.dt);
 }
 
 struct PddEq {
@@ -93,9 +129,13 @@ struct PddEq {
   double amp, inv_scale, inv_scale2, D;
 };
 
-__device__ inline double pdd_f(const PddEq& E, double u) {
-  double r = E.b[E.degree];
-  for (int k = E.degree - 1; k >= 0; --k) r = fma(r, u, E.b[k]);
+// f(u) by Horner over all nine coefficients (b_k = 0 above the degree; the
+// leading zeros add exact zeros): unrolled, the coefficients read from the
+// kernel's constant parameters — no dynamically indexed local copy
+__device__ __forceinline__ double pdd_f(const PddEq& E, double u) {
+  double r = E.b[8];
+#pragma unroll
+  for (int k = 7; k >= 0; --k) r = fma(r, u, E.b[k]);
   return r;
 }
 
@@ -122,7 +162,7 @@ __device__ inline double pdd_g(const PddEq& E, double x, double y) {
 // [4][m+1], the Thomas factors of (I - r/2 δ²) [m].  Writes its nodes of the
 // global field F[(n+1)^2] (index [i][j] global).
 __global__ void pdd_adi_kernel(const double* __restrict__ W, double* __restrict__ F, PddGeom G,
-                               PddEq E) {
+                               const __grid_constant__ PddEq E) {
   extern __shared__ double sm[];
   const int m = G.m, mm = m + 1;
   const int qx = blockIdx.x & 1, qy = blockIdx.x >> 1;

@@ -90,7 +90,7 @@ struct rt_handle {
   bool have_timing = false;
   bool scratch_used = false;   // ev[2] marks the last use of the scratch on last_stream
   double host_total_ms = -1.0;
-  DevBuf partials, gpool, gaux, lacc, wtime, sh_tsum, sh_leaves, sh_sorted, sh_boff, pdd_pts, pdd_nodal, pdd_bc, pdd_field, pdd_c, pdd_u, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
+  DevBuf partials, gpool, gaux, lacc, wtime, sh_tsum, sh_leaves, sh_sorted, sh_boff, pdd_pts, pdd_nodal, pdd_bc, pdd_field, pdd_c, pdd_u, pdd_spl, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
   int32_t grid_override = 0;
   int64_t tpt_override = 0;
   int32_t pool_override = 0;
@@ -227,7 +227,7 @@ extern "C" rt_status rt_destroy(rt_handle* h) {
   if (h->own_stream) cudaStreamSynchronize(h->own_stream);
   if (h->last_stream) cudaStreamSynchronize(h->last_stream);
   for (DevBuf* b : {&h->partials, &h->gpool, &h->gaux, &h->lacc, &h->wtime, &h->sh_tsum, &h->sh_leaves, &h->sh_sorted, &h->sh_boff, &h->pdd_pts, &h->pdd_nodal,
-                    &h->pdd_bc, &h->pdd_field, &h->pdd_c, &h->pdd_u, &h->sums, &h->stats, &h->h_points, &h->h_coeffs,
+                    &h->pdd_bc, &h->pdd_field, &h->pdd_c, &h->pdd_u, &h->pdd_spl, &h->sums, &h->stats, &h->h_points, &h->h_coeffs,
                     &h->h_stderr, &h->h_aux, &h->h_flags})
     b->release();
   for (int q = 0; q < 4; ++q)
@@ -1084,8 +1084,16 @@ static rt_status pdd_downstream(rt_handle* h, const rt_pdd_cfg* cfg, const doubl
     RT_CUDA(h->pdd_bc.ensure(static_cast<size_t>(6) * (G.n_steps + 1) * (G.n + 1) * sizeof(double)));
     bc = static_cast<double*>(h->pdd_bc.p);
   }
+  // spline scratch: Ms [6][nt][ns], A and At [6][nt][n+1]
+  RT_CUDA(h->pdd_spl.ensure((static_cast<size_t>(6) * G.nt * G.ns +
+                             static_cast<size_t>(12) * G.nt * (G.n + 1)) * sizeof(double)));
+  double* Ms = static_cast<double*>(h->pdd_spl.p);
+  double* A = Ms + static_cast<size_t>(6) * G.nt * G.ns;
+  double* At = A + static_cast<size_t>(6) * G.nt * (G.n + 1);
+  rtk::pdd_spline_s_kernel<<<(6 * G.nt + 63) / 64, 64, 0, st>>>(d_nodal, Ms, G, 6);
+  RT_CUDA(cudaGetLastError());
   const int nthr = 6 * (G.n + 1);
-  rtk::pdd_spline_kernel<<<(nthr + 127) / 128, 128, 0, st>>>(d_nodal, bc, G, 6);
+  rtk::pdd_spline_t_kernel<<<(nthr + 127) / 128, 128, 0, st>>>(d_nodal, Ms, A, At, bc, G, 6);
   RT_CUDA(cudaGetLastError());
   RT_CUDA(cudaEventRecord(h->ev[3], st));
   const int smem = rtk::pdd_smem_bytes(G.m);
