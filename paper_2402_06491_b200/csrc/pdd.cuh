@@ -157,6 +157,54 @@ __device__ inline double pdd_g(const PddEq& E, double x, double y) {
   }
 }
 
+constexpr int kPcrLevels = 6;   // cyclic reduction for up to 64 unknowns per line
+
+// shared memory of pdd_adi_kernel: u, u* [(m+1)²], edges [8][m+1], Thomas
+// factors [2][m+1], PCR multipliers [6][128] + [64], the next edge data
+// [4][m+1], PCR scratch [3][64]
+__host__ __device__ constexpr int pdd_smem_doubles(int m) {
+  return 2 * (m + 1) * (m + 1) + 8 * (m + 1) + 2 * (m + 1) + kPcrLevels * 128 + 64 + 4 * (m + 1);
+}
+__host__ __device__ constexpr int pdd_smem_bytes(int m) {
+  return (pdd_smem_doubles(m) + 3 * 64) * 8;   // + pcr_factors' scratch
+}
+
+// Elimination multipliers of parallel cyclic reduction for the constant
+// tridiagonal matrix tridiag(a, b, a) of size n <= 64 (every line of every
+// step shares it): at level lv (stride δ = 2^lv) equation i becomes
+// d_i − k1_i d_{i−δ} − k2_i d_{i+δ} with k1_i = a_i/b_{i−δ}, k2_i = c_i/b_{i+δ}
+// (0 outside [0, n)), and a, b, c updated as the reduction prescribes; after
+// the last level x_i = d_i / b_i.  Written to pk [level][k1 | k2][64] and
+// [64] 1/b; uses 3 x 64 doubles of scratch.  Block-wide (barriers inside).
+__device__ inline void pcr_factors(int n, double a0, double b0, double* pk, double* scr) {
+  double* A = scr;
+  double* B = scr + 64;
+  double* C = scr + 128;
+  const int i = threadIdx.x;
+  double a = 0.0, b = 1.0, c = 0.0;
+  if (i < n) {
+    a = i > 0 ? a0 : 0.0;
+    b = b0;
+    c = i + 1 < n ? a0 : 0.0;
+  }
+  for (int lv = 0; lv < kPcrLevels; ++lv) {
+    const int dl = 1 << lv;
+    if (i < 64) { A[i] = a; B[i] = b; C[i] = c; }
+    __syncthreads();
+    if (i < 64) {
+      double k1 = 0.0, k2 = 0.0, na = 0.0, nc = 0.0, nb = b;
+      if (i < n && i - dl >= 0) { k1 = a / B[i - dl]; na = -A[i - dl] * k1; nb -= C[i - dl] * k1; }
+      if (i < n && i + dl < n) { k2 = c / B[i + dl]; nc = -C[i + dl] * k2; nb -= A[i + dl] * k2; }
+      pk[lv * 128 + i] = k1;
+      pk[lv * 128 + 64 + i] = k2;
+      a = na; b = nb; c = nc;
+    }
+    __syncthreads();
+  }
+  if (i < 64) pk[kPcrLevels * 128 + i] = 1.0 / b;
+  __syncthreads();
+}
+
 // One CTA per subdomain q = qx + 2 qy.  Shared memory: u, u* [(m+1)^2] with
 // index [i][j] = (x_i, y_j) of the subdomain, the four edges' bB and bM
 // [4][m+1], the Thomas factors of (I - r/2 δ²) [m].  Writes its nodes of the
@@ -172,7 +220,11 @@ __global__ void pdd_adi_kernel(const double* __restrict__ W, double* __restrict_
   double* eM = eB + 4 * mm;          // [4][mm]
   double* cp = eM + 4 * mm;          // [mm] Thomas: c'_i
   double* piv = cp + mm;             // [mm] Thomas: 1/(b - a c'_{i-1})
+  double* pk = piv + mm;             // PCR: [kPcrLevels][2][64] k1, k2 per level, [64] 1/b
+  double* wN = pk + kPcrLevels * 128 + 64;   // [4][mm] W(t_{n+1}) on the four edges
   const int tid = threadIdx.x, nth = blockDim.x;
+  const int nu = m - 1;              // interior unknowns per line
+  const bool pcr = nu <= 64;         // warp-per-line cyclic reduction (else Thomas)
   const int i0 = qx * m, j0 = qy * m;             // global offsets
   // edge lines of this subdomain (see the header)
   const int lx0 = qx == 0 ? 2 : 0, lx1 = qx == 0 ? 0 : 3;
@@ -189,11 +241,70 @@ __global__ void pdd_adi_kernel(const double* __restrict__ W, double* __restrict_
       cp[k] = (-0.5 * r) * piv[k];
     }
   }
+  if (pcr) pcr_factors(nu, -0.5 * r, 1.0 + r, pk, sm + pdd_smem_doubles(m));   // (+ scratch)
+  // the edge data of the step's end, W(t_{n+1}): edge e = tid / mm (0 x0,
+  // 1 x1, 2 y0, 3 y1), loaded at the step's start (the latency overlaps the
+  // first reaction) and used twice — bB and the new boundary
+  auto w_next = [&](int n) -> double {
+    if (tid >= 4 * mm) return 0.0;
+    const int e = tid / mm, k = tid - e * mm;
+    const int line = e == 0 ? lx0 : (e == 1 ? lx1 : (e == 2 ? ly0 : ly1));
+    return Wat(line, n + 1, (e < 2 ? j0 : i0) + k);
+  };
+  // pointwise reaction R_{dt/2} on the whole subdomain, four independent
+  // points per thread in flight (the RK4 stages are a serial chain)
+  auto react = [&](double* w, double hh) {
+    for (int q0 = tid; q0 < mm * mm; q0 += 4 * nth) {
+      double v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = q0 + c * nth < mm * mm ? w[q0 + c * nth] : 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = pdd_rk4(E, v[c], hh);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (q0 + c * nth < mm * mm) w[q0 + c * nth] = v[c];
+    }
+  };
   for (int q = tid; q < mm * mm; q += nth) {      // u(x, y, 0) = g
     const int i = q / mm, j = q - i * mm;
     u[q] = pdd_g(E, G.lo + (i0 + i) * G.h, G.lo + (j0 + j) * G.h);
   }
   __syncthreads();
+  // one line's solve of (I - r/2 δ²) w = d by cyclic reduction in a warp:
+  // lane l holds unknowns l and l + 32; the elimination multipliers depend
+  // only on the (constant) matrix, so they come precomputed (pcr_factors)
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nth >> 5;
+  auto pcr_solve = [&](double& d0, double& d1) {
+    // levels with compile-time strides; a level whose stride reaches nu is
+    // a no-op (its multipliers are 0) and is skipped
+#pragma unroll
+    for (int lv = 0; lv < kPcrLevels; ++lv) {
+      constexpr int kW = 32;
+      const int dl = 1 << lv;
+      if (dl >= nu) break;                        // (uniform)
+      const double* k1 = pk + lv * 128;
+      const double* k2 = k1 + 64;
+      double lo0, lo1, hi0, hi1;
+      if (dl < kW) {
+        const double a0 = __shfl_up_sync(0xffffffffu, d0, dl), a1 = __shfl_up_sync(0xffffffffu, d1, dl);
+        const double w0 = __shfl_down_sync(0xffffffffu, d0, dl), w1 = __shfl_down_sync(0xffffffffu, d1, dl);
+        const double c0 = __shfl_sync(0xffffffffu, d0, (lane - dl) & 31);   // e1's lower across the halves
+        const double c1 = __shfl_sync(0xffffffffu, d1, (lane + dl) & 31);   // e0's upper across the halves
+        const bool dn = lane >= dl, up = lane + dl < kW;
+        lo0 = dn ? a0 : 0.0;
+        lo1 = dn ? a1 : c0;
+        hi0 = up ? w0 : c1;
+        hi1 = up ? w1 : 0.0;
+      } else {                                   // dl = 32: e0 <-> e1 of the same lane
+        lo0 = 0.0; lo1 = d0; hi0 = d1; hi1 = 0.0;
+      }
+      // (multipliers are 0 where the neighbour is outside [0, nu))
+      d0 = fma(-k2[lane], hi0, fma(-k1[lane], lo0, d0));
+      d1 = fma(-k2[lane + 32], hi1, fma(-k1[lane + 32], lo1, d1));
+    }
+    d0 *= pk[kPcrLevels * 128 + lane];
+    d1 *= pk[kPcrLevels * 128 + lane + 32];
+  };
   auto impose = [&](double* w, int st) {           // boundary = W at step st
     for (int k = tid; k < mm; k += nth) {
       w[0 * mm + k] = Wat(lx0, st, j0 + k);
@@ -208,14 +319,16 @@ __global__ void pdd_adi_kernel(const double* __restrict__ W, double* __restrict_
   };
   impose(u, 0);
   for (int n = 0; n < G.n_steps; ++n) {
-    for (int q = tid; q < mm * mm; q += nth) u[q] = pdd_rk4(E, u[q], 0.5 * G.dt);   // -> bA
+    const double wv = w_next(n);
+    react(u, 0.5 * G.dt);                                                   // -> bA
+    if (tid < 4 * mm) wN[tid] = wv;
     __syncthreads();
     // bB = R_{-dt/2} W(t_{n+1}); bM = (bA + bB)/2, per edge
     for (int k = tid; k < mm; k += nth) {
-      const double b0 = pdd_rk4(E, Wat(lx0, n + 1, j0 + k), -0.5 * G.dt);
-      const double b1 = pdd_rk4(E, Wat(lx1, n + 1, j0 + k), -0.5 * G.dt);
-      const double b2 = pdd_rk4(E, Wat(ly0, n + 1, i0 + k), -0.5 * G.dt);
-      const double b3 = pdd_rk4(E, Wat(ly1, n + 1, i0 + k), -0.5 * G.dt);
+      const double b0 = pdd_rk4(E, wN[0 * mm + k], -0.5 * G.dt);
+      const double b1 = pdd_rk4(E, wN[1 * mm + k], -0.5 * G.dt);
+      const double b2 = pdd_rk4(E, wN[2 * mm + k], -0.5 * G.dt);
+      const double b3 = pdd_rk4(E, wN[3 * mm + k], -0.5 * G.dt);
       eB[0 * mm + k] = b0; eB[1 * mm + k] = b1; eB[2 * mm + k] = b2; eB[3 * mm + k] = b3;
       eM[0 * mm + k] = 0.5 * (u[0 * mm + k] + b0);
       eM[1 * mm + k] = 0.5 * (u[m * mm + k] + b1);
@@ -225,16 +338,29 @@ __global__ void pdd_adi_kernel(const double* __restrict__ W, double* __restrict_
     __syncthreads();
     // x-sweep: row j (thread), unknowns i = 1..m-1:
     // (I - r/2 δx²) u* = (I + r/2 δy²) u with u* = bM on the x edges
-    for (int j = 1 + tid; j <= m - 1; j += nth) {
-      double prev = 0.0;
-      for (int i = 1; i <= m - 1; ++i) {
-        double d = u[i * mm + j] + 0.5 * r * (u[i * mm + j - 1] - 2.0 * u[i * mm + j] + u[i * mm + j + 1]);
-        if (i == 1) d += 0.5 * r * eM[0 * mm + j];
-        if (i == m - 1) d += 0.5 * r * eM[1 * mm + j];
-        prev = (i == 1) ? d * piv[i] : (d - (-0.5 * r) * prev) * piv[i];
-        us[i * mm + j] = prev;                      // forward pass: d'_i
+    auto dx = [&](int i, int j) -> double {
+      double d = u[i * mm + j] + 0.5 * r * (u[i * mm + j - 1] - 2.0 * u[i * mm + j] + u[i * mm + j + 1]);
+      if (i == 1) d += 0.5 * r * eM[0 * mm + j];
+      if (i == m - 1) d += 0.5 * r * eM[1 * mm + j];
+      return d;
+    };
+    if (pcr) {
+      for (int j = 1 + warp; j <= m - 1; j += nwarp) {   // a warp per row
+        double d0 = lane < nu ? dx(lane + 1, j) : 0.0;
+        double d1 = lane + 32 < nu ? dx(lane + 33, j) : 0.0;
+        pcr_solve(d0, d1);
+        if (lane < nu) us[(lane + 1) * mm + j] = d0;
+        if (lane + 32 < nu) us[(lane + 33) * mm + j] = d1;
       }
-      for (int i = m - 2; i >= 1; --i) us[i * mm + j] -= cp[i] * us[(i + 1) * mm + j];
+    } else {
+      for (int j = 1 + tid; j <= m - 1; j += nth) {
+        double prev = 0.0;
+        for (int i = 1; i <= m - 1; ++i) {
+          prev = (i == 1) ? dx(i, j) * piv[i] : (dx(i, j) - (-0.5 * r) * prev) * piv[i];
+          us[i * mm + j] = prev;                    // forward pass: d'_i
+        }
+        for (int i = m - 2; i >= 1; --i) us[i * mm + j] -= cp[i] * us[(i + 1) * mm + j];
+      }
     }
     for (int k = tid; k < mm; k += nth) {           // u* boundary = bM
       us[0 * mm + k] = eM[0 * mm + k];
@@ -248,16 +374,29 @@ __global__ void pdd_adi_kernel(const double* __restrict__ W, double* __restrict_
     __syncthreads();
     // y-sweep: column i (thread), unknowns j = 1..m-1:
     // (I - r/2 δy²) v = (I + r/2 δx²) u* with v = bB on the y edges
-    for (int i = 1 + tid; i <= m - 1; i += nth) {
-      double prev = 0.0;
-      for (int j = 1; j <= m - 1; ++j) {
-        double d = us[i * mm + j] + 0.5 * r * (us[(i - 1) * mm + j] - 2.0 * us[i * mm + j] + us[(i + 1) * mm + j]);
-        if (j == 1) d += 0.5 * r * eB[2 * mm + i];
-        if (j == m - 1) d += 0.5 * r * eB[3 * mm + i];
-        prev = (j == 1) ? d * piv[j] : (d - (-0.5 * r) * prev) * piv[j];
-        u[i * mm + j] = prev;
+    auto dy = [&](int i, int j) -> double {
+      double d = us[i * mm + j] + 0.5 * r * (us[(i - 1) * mm + j] - 2.0 * us[i * mm + j] + us[(i + 1) * mm + j]);
+      if (j == 1) d += 0.5 * r * eB[2 * mm + i];
+      if (j == m - 1) d += 0.5 * r * eB[3 * mm + i];
+      return d;
+    };
+    if (pcr) {
+      for (int i = 1 + warp; i <= m - 1; i += nwarp) {   // a warp per column
+        double d0 = lane < nu ? dy(i, lane + 1) : 0.0;
+        double d1 = lane + 32 < nu ? dy(i, lane + 33) : 0.0;
+        pcr_solve(d0, d1);
+        if (lane < nu) u[i * mm + lane + 1] = d0;
+        if (lane + 32 < nu) u[i * mm + lane + 33] = d1;
       }
-      for (int j = m - 2; j >= 1; --j) u[i * mm + j] -= cp[j] * u[i * mm + j + 1];
+    } else {
+      for (int i = 1 + tid; i <= m - 1; i += nth) {
+        double prev = 0.0;
+        for (int j = 1; j <= m - 1; ++j) {
+          prev = (j == 1) ? dy(i, j) * piv[j] : (dy(i, j) - (-0.5 * r) * prev) * piv[j];
+          u[i * mm + j] = prev;
+        }
+        for (int j = m - 2; j >= 1; --j) u[i * mm + j] -= cp[j] * u[i * mm + j + 1];
+      }
     }
     __syncthreads();
     for (int k = tid; k < mm; k += nth) {           // v boundary = bB
@@ -270,9 +409,18 @@ __global__ void pdd_adi_kernel(const double* __restrict__ W, double* __restrict_
       u[k * mm + m] = eB[3 * mm + k];
     }
     __syncthreads();
-    for (int q = tid; q < mm * mm; q += nth) u[q] = pdd_rk4(E, u[q], 0.5 * G.dt);
+    react(u, 0.5 * G.dt);
     __syncthreads();
-    impose(u, n + 1);
+    for (int k = tid; k < mm; k += nth) {          // boundary = W(t_{n+1})
+      u[0 * mm + k] = wN[0 * mm + k];
+      u[m * mm + k] = wN[1 * mm + k];
+    }
+    __syncthreads();
+    for (int k = tid; k < mm; k += nth) {
+      u[k * mm + 0] = wN[2 * mm + k];
+      u[k * mm + m] = wN[3 * mm + k];
+    }
+    __syncthreads();
   }
   for (int q = tid; q < mm * mm; q += nth) {
     const int i = q / mm, j = q - i * mm;
@@ -280,8 +428,5 @@ __global__ void pdd_adi_kernel(const double* __restrict__ W, double* __restrict_
   }
 }
 
-__host__ __device__ constexpr int pdd_smem_bytes(int m) {
-  return (2 * (m + 1) * (m + 1) + 8 * (m + 1) + 2 * (m + 1)) * 8;
-}
 
 }  // namespace rtk
