@@ -20,7 +20,7 @@ import bench  # noqa: E402
 import paper_2402_06491_b200 as P  # noqa: E402
 import workloads as W  # noqa: E402
 
-NAMES = ("ex1A", "ex1B", "ex3A", "ex3B", "ex5A", "ex5B", "cfg2", "cfg3", "cfg4",
+NAMES = ("ex1A", "ex1B", "ex2A", "ex2B", "ex3A", "ex3B", "ex5A", "ex5B", "cfg2", "cfg3", "cfg4",
          "cfg2_sh", "cfg3_sh", "cfg4_sh")
 
 

@@ -65,8 +65,9 @@ def main():
             f.write(json.dumps(r) + "\n")
     md = ["# cfg5 throughput sweep (1 x B200, tree-walk launch time)", "",
           "cfg2 equation, d = 1, g = 0.4 exp(-x^2), K = 12; nodes linspace(-3, 3, n).  "
-          "frac = algorithmic FP64 lane-ops (bench.py cost model) / (148 x 64 x 1.965 GHz); for the "
-          "FP32-position variant the same algorithmic count is used (same method, less FP64 work).", "",
+          "frac = algorithmic FP64 lane-ops (bench.py cost model: R29 contract units, DESIGN.md §5) / "
+          "(148 x 64 x 1.965 GHz); the FP32-position variant is credited only its FP64 part (clock, "
+          "weights, product, sums), so its frac is not comparable with the FP64 rows — compare trees/s.", "",
           "| precision | t | nodes | trees/node | launch ms | trees/s | leaf-evals/s | particles/tree | pruned | frac |",
           "|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
