@@ -624,8 +624,10 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   const bool sh = p.shared != 0;
   bool var = false;
   for (int k = 0; k <= 8; ++k) var = var || p.coef_kind[k] != RT_COEF_CONST;
-  // the general kernel only where f2/f3 weight factors or > 3 offspring kinds need it
-  const bool gen = p.strategy != RT_STRATEGY_POTENTIAL || var || nz.n_support > 3;
+  // the general kernel only where f2/f3 weight factors, > 3 offspring kinds or
+  // an empty support (purely linear f) need it
+  const bool gen = p.strategy != RT_STRATEGY_POTENTIAL || var || nz.n_support > 3 ||
+                   nz.n_support == 0;
   KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, p.precision == RT_PREC_FP32_POS,
                            p.strategy == RT_STRATEGY_B, sh, gen, &prod, &smem, &pool_cap);
   if (!fn) return fail(RT_E_ARG, "no kernel for dim=%d init_kind=%d", p.dim, p.init_kind);

@@ -244,7 +244,7 @@ __device__ __forceinline__ void red_add_keep(double* p, double v, uint64_t pol) 
 // each tree's summary (TreeSum) and leaf displacements; phase 2
 // (shared_eval.cuh) evaluates all nodes.  Constant coefficients only.
 // GEN = false: the common equations — no f2/f3 weight factors (wmode = 0)
-// and at most three offspring kinds — without the warp-uniform tests for the
+// and one to three offspring kinds — without the warp-uniform tests for the
 // rest (the same arithmetic; chosen by the launcher).
 template <int DIM, int GK, bool REC, bool F32, bool SB, bool SH, bool GEN = true>
 __global__ void __launch_bounds__(kThreads, MinCtas<DIM, REC>::v)
@@ -589,7 +589,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const bool pruned = split && ne > P.K;       // prune
     // a pruned tree (ne = K+1, the pruned bin) and a killed one (purely linear
     // f: no offspring, bin ne) both end here with a zero product
-    const bool dead = split && (ne > P.K || P.n_support == 0);
+    const bool dead = split && (ne > P.K || (GEN && P.n_support == 0));   // (GEN = false: support non-empty)
     const bool branch = split && !dead;
     // g at a leaf; h^(α) = c'_α at a split
     const double gl = SH ? 1.0 : gv;            // SH: g is applied per node below
