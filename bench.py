@@ -325,11 +325,20 @@ def main():
     import paper_2402_06491_b200 as P
 
     ws, rank, local = _dist()
+    # (RT_BENCH_DRY_MULTI=1: a dry run of the N > 1 logic with every rank on
+    # cuda:0 and gloo collectives — the multi-rank code path exercised on a
+    # 1-GPU box; never a measurement)
+    dry = os.environ.get("RT_BENCH_DRY_MULTI") == "1"
+    if dry:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if dry:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     eq, t, N, seed = cfg["eq"], cfg["t"], cfg["n_trees"], cfg["seed"]
     K, L, M = eq["K"], cfg["L"], cfg["M"]
     pts = W.nodes(cfg)
