@@ -351,28 +351,48 @@ static rt_status plan_launch(rt_handle* h, KernelFn fn, int smem, int64_t n_poin
   return RT_OK;
 }
 
-__global__ void reduce_tasks_kernel(const double* __restrict__ partials, int64_t tpn, int nb,
-                                    double* __restrict__ sums,
-                                    unsigned long long* __restrict__ stats) {
-  // second pass: node i's tasks summed in task order (atomic-free, deterministic);
-  // the exact bin counts also give trees, pruned trees and splits (a pruned
-  // tree aborted at its (K+1)-th split)
+constexpr int kReduceWarps = 8;
+
+__global__ void __launch_bounds__(32 * kReduceWarps)
+reduce_tasks_kernel(const double* __restrict__ partials, int64_t tpn, int nb,
+                    double* __restrict__ sums, unsigned long long* __restrict__ stats) {
+  // second pass, atomic-free and deterministic: node i's tasks are summed by
+  // eight warps — warp w takes tasks w, w+8, w+16, … in ascending order, lane
+  // = bin — and the eight partial sums are added in warp order; the exact bin
+  // counts also give trees, pruned trees and splits (a pruned tree aborted at
+  // its (K+1)-th split)
+  __shared__ double part[kReduceWarps][32][3];
   const int64_t i = blockIdx.x;
-  const int b = threadIdx.x;
+  const int b = threadIdx.x & 31, w = threadIdx.x >> 5;
   double s1 = 0.0, s2 = 0.0, c = 0.0;
   if (b < nb) {
-    const double* p = partials + (i * tpn * nb + b) * 3;
-    for (int64_t q = 0; q < tpn; ++q, p += static_cast<int64_t>(nb) * 3) {
+    const int64_t st = static_cast<int64_t>(nb) * 3;
+    const double* p = partials + (i * tpn * nb + b) * 3 + w * st;
+    for (int64_t q = w; q < tpn; q += kReduceWarps, p += kReduceWarps * st) {
       s1 += p[0];
       s2 += p[1];
       c += p[2];
     }
+  }
+  part[w][b][0] = s1;
+  part[w][b][1] = s2;
+  part[w][b][2] = c;
+  __syncthreads();
+  if (w != 0) return;
+  s1 = s2 = c = 0.0;
+#pragma unroll
+  for (int v = 0; v < kReduceWarps; ++v) {
+    s1 += part[v][b][0];
+    s2 += part[v][b][1];
+    c += part[v][b][2];
+  }
+  if (b < nb) {
     double* o = sums + (i * nb + b) * 3;
     o[0] = s1;
     o[1] = s2;
     o[2] = c;
   }
-  unsigned long long trees = static_cast<unsigned long long>(c);
+  unsigned long long trees = b < nb ? static_cast<unsigned long long>(c) : 0ull;
   unsigned long long splits = trees * static_cast<unsigned long long>(b);
   for (int o = 16; o > 0; o >>= 1) {
     trees += __shfl_xor_sync(0xffffffffu, trees, o);
@@ -600,7 +620,7 @@ static rt_status run_walk_shared(rt_handle* h, KernelFn prod, int smem, int pool
     q0 += eg.y;
   }
   RT_CUDA(cudaEventRecord(h->ev[1], st));
-  reduce_tasks_kernel<<<static_cast<unsigned>(n_points), 32, 0, st>>>(
+  reduce_tasks_kernel<<<static_cast<unsigned>(n_points), 32 * kReduceWarps, 0, st>>>(
       static_cast<double*>(h->partials.p), tpn_total, nb, d_sums,
       static_cast<unsigned long long*>(h->stats.p));
   RT_CUDA(cudaGetLastError());
@@ -697,7 +717,7 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
     }
   }
   RT_CUDA(cudaEventRecord(h->ev[1], st));
-  reduce_tasks_kernel<<<static_cast<unsigned>(n_points), 32, 0, st>>>(
+  reduce_tasks_kernel<<<static_cast<unsigned>(n_points), 32 * kReduceWarps, 0, st>>>(
       static_cast<double*>(h->partials.p), L.tpn, nb, d_sums,
       static_cast<unsigned long long*>(h->stats.p));
   RT_CUDA(cudaGetLastError());
