@@ -20,6 +20,7 @@
 // t_k = k T/(nt - 1).  Boundary table W[line][step][i] at (s = x_i, t_step).
 #pragma once
 #include <cstdint>
+#include <cooperative_groups.h>
 
 namespace rtk {
 
@@ -318,22 +319,25 @@ __global__ void pdd_adi_kernel(const double* __restrict__ W, double* __restrict_
     __syncthreads();
   };
   impose(u, 0);
+  // bM's edge value of u after the first reaction: edge e = tid / mm
+  auto u_edge = [&](const double* w) -> double {
+    const int e = tid / mm, k = tid - e * mm;
+    return e == 0 ? w[k] : (e == 1 ? w[m * mm + k] : (e == 2 ? w[k * mm] : w[k * mm + m]));
+  };
+  double w_ahead = w_next(0);                       // W(t_1), one step ahead
   for (int n = 0; n < G.n_steps; ++n) {
-    const double wv = w_next(n);
+    // bB = R_{-dt/2} W(t_{n+1}) — independent of u: one edge value per
+    // thread, computed alongside the first reaction; W(t_{n+2}) is loaded a
+    // whole step before its use (its latency hidden behind the step)
+    const double wv = w_ahead;
+    if (n + 1 < G.n_steps) w_ahead = w_next(n + 1);
+    const double bv = tid < 4 * mm ? pdd_rk4(E, wv, -0.5 * G.dt) : 0.0;
     react(u, 0.5 * G.dt);                                                   // -> bA
-    if (tid < 4 * mm) wN[tid] = wv;
     __syncthreads();
-    // bB = R_{-dt/2} W(t_{n+1}); bM = (bA + bB)/2, per edge
-    for (int k = tid; k < mm; k += nth) {
-      const double b0 = pdd_rk4(E, wN[0 * mm + k], -0.5 * G.dt);
-      const double b1 = pdd_rk4(E, wN[1 * mm + k], -0.5 * G.dt);
-      const double b2 = pdd_rk4(E, wN[2 * mm + k], -0.5 * G.dt);
-      const double b3 = pdd_rk4(E, wN[3 * mm + k], -0.5 * G.dt);
-      eB[0 * mm + k] = b0; eB[1 * mm + k] = b1; eB[2 * mm + k] = b2; eB[3 * mm + k] = b3;
-      eM[0 * mm + k] = 0.5 * (u[0 * mm + k] + b0);
-      eM[1 * mm + k] = 0.5 * (u[m * mm + k] + b1);
-      eM[2 * mm + k] = 0.5 * (u[k * mm + 0] + b2);
-      eM[3 * mm + k] = 0.5 * (u[k * mm + m] + b3);
+    if (tid < 4 * mm) {                                                     // bM = (bA + bB)/2
+      wN[tid] = wv;
+      eB[tid] = bv;
+      eM[tid] = 0.5 * (u_edge(u) + bv);
     }
     __syncthreads();
     // x-sweep: row j (thread), unknowns i = 1..m-1:
@@ -428,5 +432,220 @@ __global__ void pdd_adi_kernel(const double* __restrict__ W, double* __restrict_
   }
 }
 
+
+// The same local solver with each subdomain spread over a thread-block
+// CLUSTER of kPddCluster CTAs (one SM each; 4 x 8 = 32 SMs instead of 4),
+// for lines of up to 64 unknowns.  Every CTA keeps full copies of u and u*
+// in its shared memory; CTA c of a cluster owns the rows j ≡ c (mod C) (the
+// reactions and the x-direction line solves) and the columns i ≡ c (the
+// y-direction line solves), and writes every value it computes into all C
+// copies through distributed shared memory (st.shared::cluster), one cluster
+// barrier after each of the four phases of a step.  The edge data, their
+// R_{±dt/2} transforms and the line-solve multipliers are computed by every
+// CTA redundantly (identical arithmetic), and the new step's boundary values
+// W(t_{n+1}) are folded into the first reaction of the next step, so no
+// phase writes a value another CTA may still be reading.  The arithmetic of
+// every value is the single-CTA kernel's: the fields agree bit for bit.
+constexpr int kPddCluster = 8;
+
+__host__ __device__ constexpr int pdd_cluster_smem_doubles(int m) {
+  return 2 * (m + 1) * (m + 1) + 8 * (m + 1) + kPcrLevels * 128 + 64 + 8 * (m + 1);
+}
+__host__ __device__ constexpr int pdd_cluster_smem_bytes(int m) {
+  return (pdd_cluster_smem_doubles(m) + 3 * 64) * 8;
+}
+
+__global__ void pdd_adi_cluster_kernel(const double* __restrict__ W, double* __restrict__ F, PddGeom G,
+                                       const __grid_constant__ PddEq E) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double sm[];
+  const int C = static_cast<int>(cl.num_blocks());
+  const int crank = static_cast<int>(cl.block_rank());
+  const int sub = blockIdx.x / C;                 // subdomain q = qx + 2 qy
+  const int m = G.m, mm = m + 1, nu = m - 1;
+  const int qx = sub & 1, qy = sub >> 1;
+  double* u = sm;                    // [mm][mm] full copy
+  double* us = u + mm * mm;          // [mm][mm] full copy
+  double* eB = us + mm * mm;         // [4][mm]
+  double* eM = eB + 4 * mm;          // [4][mm]
+  double* pk = eM + 4 * mm;          // PCR multipliers [6][128] + [64]
+  double* wN = pk + kPcrLevels * 128 + 64;   // [4][mm] W(t_{n+1})
+  double* wB = wN + 4 * mm;                  // [4][mm] W(t_n): this step's boundary
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nth >> 5;
+  const int i0 = qx * m, j0 = qy * m;
+  const int lx0 = qx == 0 ? 2 : 0, lx1 = qx == 0 ? 0 : 3;
+  const int ly0 = qy == 0 ? 4 : 1, ly1 = qy == 0 ? 1 : 5;
+  const int64_t lstride = static_cast<int64_t>(G.n_steps + 1) * (G.n + 1);
+  auto Wat = [&](int line, int st, int gi) -> double {
+    return W[line * lstride + static_cast<int64_t>(st) * (G.n + 1) + gi];
+  };
+  auto w_at = [&](int st) -> double {            // edge e = tid / mm of W(t_st)
+    if (tid >= 4 * mm) return 0.0;
+    const int e = tid / mm, k = tid - e * mm;
+    const int line = e == 0 ? lx0 : (e == 1 ? lx1 : (e == 2 ? ly0 : ly1));
+    return Wat(line, st, (e < 2 ? j0 : i0) + k);
+  };
+  const double r = E.D * G.dt / (G.h * G.h);
+  pcr_factors(nu, -0.5 * r, 1.0 + r, pk, sm + pdd_cluster_smem_doubles(m));
+  // remote copies: the same offset in every CTA of the cluster
+  auto put = [&](double* base, int off, double v) {
+    for (int c = 0; c < C; ++c) cl.map_shared_rank(base, c)[off] = v;
+  };
+  // the value at (i, j) at the start of a step: the boundary is W(t_n) (the
+  // y-edges over the x-edges at the corners, as the single-CTA impose)
+  auto start_val = [&](int i, int j) -> double {
+    if (j == 0) return wB[2 * mm + i];
+    if (j == m) return wB[3 * mm + i];
+    if (i == 0) return wB[0 * mm + j];
+    if (i == m) return wB[1 * mm + j];
+    return u[i * mm + j];
+  };
+  {                                              // u(x, y, 0) = g; W(t_0)
+    const double w0 = w_at(0);
+    for (int q = tid; q < mm * mm; q += nth) {
+      const int i = q / mm, j = q - i * mm;
+      u[q] = pdd_g(E, G.lo + (i0 + i) * G.h, G.lo + (j0 + j) * G.h);
+    }
+    if (tid < 4 * mm) wB[tid] = w0;
+  }
+  cl.sync();
+  auto pcr_solve = [&](double& d0, double& d1) {
+#pragma unroll
+    for (int lv = 0; lv < kPcrLevels; ++lv) {
+      const int dl = 1 << lv;
+      if (dl >= nu) break;
+      const double* k1 = pk + lv * 128;
+      const double* k2 = k1 + 64;
+      double lo0, lo1, hi0, hi1;
+      if (dl < 32) {
+        const double a0 = __shfl_up_sync(0xffffffffu, d0, dl), a1 = __shfl_up_sync(0xffffffffu, d1, dl);
+        const double w0 = __shfl_down_sync(0xffffffffu, d0, dl), w1 = __shfl_down_sync(0xffffffffu, d1, dl);
+        const double c0 = __shfl_sync(0xffffffffu, d0, (lane - dl) & 31);
+        const double c1 = __shfl_sync(0xffffffffu, d1, (lane + dl) & 31);
+        const bool dn = lane >= dl, up = lane + dl < 32;
+        lo0 = dn ? a0 : 0.0;
+        lo1 = dn ? a1 : c0;
+        hi0 = up ? w0 : c1;
+        hi1 = up ? w1 : 0.0;
+      } else {
+        lo0 = 0.0; lo1 = d0; hi0 = d1; hi1 = 0.0;
+      }
+      d0 = fma(-k2[lane], hi0, fma(-k1[lane], lo0, d0));
+      d1 = fma(-k2[lane + 32], hi1, fma(-k1[lane + 32], lo1, d1));
+    }
+    d0 *= pk[kPcrLevels * 128 + lane];
+    d1 *= pk[kPcrLevels * 128 + lane + 32];
+  };
+  // owned points (i, j), j ≡ crank (mod C): four in flight per thread
+  const int nrow = (mm - crank + C - 1) / C;     // owned rows j = crank + C t
+  auto react_owned = [&](bool from_start, double hh) {
+    const int npt = nrow * mm;
+    if (npt <= nth) {                            // one point per thread
+      if (tid < npt) {
+        const int i = tid % mm, j = crank + C * (tid / mm);
+        put(u, i * mm + j, pdd_rk4(E, from_start ? start_val(i, j) : u[i * mm + j], hh));
+      }
+      return;
+    }
+    for (int q0 = tid; q0 < npt; q0 += 4 * nth) {
+      double v[4];
+      int ii[4], jj[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int q = q0 + c * nth;
+        ii[c] = q % mm;
+        jj[c] = crank + C * (q / mm);
+        v[c] = q < npt ? (from_start ? start_val(ii[c], jj[c]) : u[ii[c] * mm + jj[c]]) : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = pdd_rk4(E, v[c], hh);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (q0 + c * nth < npt) put(u, ii[c] * mm + jj[c], v[c]);
+    }
+  };
+  auto u_edge = [&](const double* w) -> double {
+    const int e = tid / mm, k = tid - e * mm;
+    return e == 0 ? w[k] : (e == 1 ? w[m * mm + k] : (e == 2 ? w[k * mm] : w[k * mm + m]));
+  };
+  double w_ahead = w_at(1);                          // W(t_1), one step ahead
+  for (int n = 0; n < G.n_steps; ++n) {
+    const double wv = w_ahead;
+    if (n + 1 < G.n_steps) w_ahead = w_at(n + 2);
+    const double bv = tid < 4 * mm ? pdd_rk4(E, wv, -0.5 * G.dt) : 0.0;   // bB (every CTA)
+    react_owned(true, 0.5 * G.dt);                // bA (boundary W(t_n) folded in)
+    cl.sync();
+    if (tid < 4 * mm) {                           // bM = (bA + bB)/2
+      wN[tid] = wv;
+      eB[tid] = bv;
+      eM[tid] = 0.5 * (u_edge(u) + bv);
+    }
+    __syncthreads();
+    // x-sweep, owned rows j: (I - r/2 δx²) u* = (I + r/2 δy²) u, u* = bM on the x edges
+    auto dx = [&](int i, int j) -> double {
+      double d = u[i * mm + j] + 0.5 * r * (u[i * mm + j - 1] - 2.0 * u[i * mm + j] + u[i * mm + j + 1]);
+      if (i == 1) d += 0.5 * r * eM[0 * mm + j];
+      if (i == m - 1) d += 0.5 * r * eM[1 * mm + j];
+      return d;
+    };
+    for (int t = warp; ; t += nwarp) {
+      const int j = crank + C * t;
+      if (j > m - 1) break;
+      if (j < 1) continue;
+      double d0 = lane < nu ? dx(lane + 1, j) : 0.0;
+      double d1 = lane + 32 < nu ? dx(lane + 33, j) : 0.0;
+      pcr_solve(d0, d1);
+      if (lane < nu) put(us, (lane + 1) * mm + j, d0);
+      if (lane + 32 < nu) put(us, (lane + 33) * mm + j, d1);
+    }
+    for (int k = tid; k < mm; k += nth) {         // u* boundary = bM (every CTA)
+      us[0 * mm + k] = eM[0 * mm + k];
+      us[m * mm + k] = eM[1 * mm + k];
+    }
+    __syncthreads();
+    for (int k = tid; k < mm; k += nth) {
+      us[k * mm + 0] = eM[2 * mm + k];
+      us[k * mm + m] = eM[3 * mm + k];
+    }
+    cl.sync();
+    // y-sweep, owned columns i: (I - r/2 δy²) v = (I + r/2 δx²) u*, v = bB on the y edges
+    auto dy = [&](int i, int j) -> double {
+      double d = us[i * mm + j] + 0.5 * r * (us[(i - 1) * mm + j] - 2.0 * us[i * mm + j] + us[(i + 1) * mm + j]);
+      if (j == 1) d += 0.5 * r * eB[2 * mm + i];
+      if (j == m - 1) d += 0.5 * r * eB[3 * mm + i];
+      return d;
+    };
+    for (int t = warp; ; t += nwarp) {
+      const int i = crank + C * t;
+      if (i > m - 1) break;
+      if (i < 1) continue;
+      double d0 = lane < nu ? dy(i, lane + 1) : 0.0;
+      double d1 = lane + 32 < nu ? dy(i, lane + 33) : 0.0;
+      pcr_solve(d0, d1);
+      if (lane < nu) put(u, i * mm + lane + 1, d0);
+      if (lane + 32 < nu) put(u, i * mm + lane + 33, d1);
+    }
+    for (int k = tid; k < mm; k += nth) {         // v boundary = bB (every CTA)
+      u[0 * mm + k] = eB[0 * mm + k];
+      u[m * mm + k] = eB[1 * mm + k];
+    }
+    __syncthreads();
+    for (int k = tid; k < mm; k += nth) {
+      u[k * mm + 0] = eB[2 * mm + k];
+      u[k * mm + m] = eB[3 * mm + k];
+    }
+    cl.sync();
+    react_owned(false, 0.5 * G.dt);
+    if (tid < 4 * mm) wB[tid] = wN[tid];          // the next step's boundary: W(t_{n+1})
+    cl.sync();
+  }
+  // the field at T with the final boundary W(t_N), owned rows
+  for (int q = tid; q < nrow * mm; q += nth) {
+    const int i = q % mm, j = crank + C * (q / mm);
+    F[static_cast<int64_t>(i0 + i) * (G.n + 1) + (j0 + j)] = start_val(i, j);
+  }
+}
 
 }  // namespace rtk

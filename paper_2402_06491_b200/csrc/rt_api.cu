@@ -94,6 +94,7 @@ struct rt_handle {
   int32_t grid_override = 0;
   int64_t tpt_override = 0;
   int32_t pool_override = 0;
+  bool pdd_cluster = true;   // RT_PDD_CLUSTER=0: the single-CTA local solver (A/B tests)
 };
 
 // ---------------------------------------------------------------------------
@@ -210,6 +211,7 @@ extern "C" rt_status rt_create(const rt_eq_params* params, rt_handle** out) {
     return fail(RT_E_ARG, "label width 1 + K*beta = %d exceeds 56 bits", 1 + p.K * nz.beta);
   rt_handle* h = new rt_handle();
   h->p = p;
+  if (const char* e = std::getenv("RT_PDD_CLUSTER")) h->pdd_cluster = std::atoi(e) != 0;
   h->nz = nz;
   cudaError_t e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
   for (int q = 0; q < 4 && e == cudaSuccess; ++q) e = cudaEventCreate(&h->ev[q]);
@@ -1118,6 +1120,27 @@ static rt_status pdd_downstream(rt_handle* h, const rt_pdd_cfg* cfg, const doubl
   rtk::pdd_spline_t_kernel<<<(nthr + 127) / 128, 128, 0, st>>>(d_nodal, Ms, A, At, bc, G, 6);
   RT_CUDA(cudaGetLastError());
   RT_CUDA(cudaEventRecord(h->ev[3], st));
+  if (G.m - 1 <= 64 && h->pdd_cluster) {
+    // a thread-block cluster of kPddCluster CTAs per subdomain (pdd.cuh)
+    const int smem = rtk::pdd_cluster_smem_bytes(G.m);
+    RT_CUDA(cudaFuncSetAttribute((const void*)rtk::pdd_adi_cluster_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(4 * rtk::kPddCluster);
+    lc.blockDim = dim3(256);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = rtk::kPddCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    RT_CUDA(cudaLaunchKernelEx(&lc, rtk::pdd_adi_cluster_kernel, static_cast<const double*>(bc), d_field,
+                               G, pdd_eq(h->p)));
+    return RT_OK;
+  }
   const int smem = rtk::pdd_smem_bytes(G.m);
   RT_CUDA(cudaFuncSetAttribute((const void*)rtk::pdd_adi_kernel,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -147,3 +147,23 @@ def test_pdd_solve_early_levels_degenerate_table(P, orc):
     assert fallback > 0, "no degenerate table at these sizes: the test lost its point"
     Fo, _ = PO.pdd_downstream(V, cfg, eq)
     assert np.max(np.abs(F - Fo)) <= 1e-11 * max(1.0, np.max(np.abs(Fo)))
+
+
+def test_pdd_cluster_solver_equals_single_cta(P, monkeypatch):
+    """The local solver spread over a thread-block cluster per subdomain
+    (pdd_adi_cluster_kernel, DSMEM copies) performs every value's arithmetic
+    exactly as the single-CTA kernel: the fields agree bit for bit."""
+    eq = W.get("cfg3")["eq"]
+    cfg = dict(CFG, n_cells=64, n_steps=150, n_s=9, n_t=5, lo=-1.5, hi=2.5)
+    nodes = PO.pdd_nodes(cfg)
+    rng = np.random.default_rng(5)
+    tk = cfg["T"] * np.arange(cfg["n_t"]) / (cfg["n_t"] - 1)
+    base = 0.5 * np.exp(-(nodes[..., 0] ** 2 + nodes[..., 1] ** 2))
+    V = np.stack([[base[l] * np.exp(-0.7 * t) + 0.01 * rng.normal(size=cfg["n_s"]) for t in tk]
+                  for l in range(6)])
+    Vd = torch.as_tensor(V, device="cuda")
+    F1, _ = P.Estimator(eq).pdd_downstream(cfg, Vd)            # cluster (default)
+    monkeypatch.setenv("RT_PDD_CLUSTER", "0")
+    F0, _ = P.Estimator(eq).pdd_downstream(cfg, Vd)            # one CTA per subdomain
+    torch.cuda.synchronize()
+    assert torch.equal(F1, F0)
