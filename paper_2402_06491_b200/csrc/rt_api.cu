@@ -1127,7 +1127,8 @@ static rt_status pdd_downstream(rt_handle* h, const rt_pdd_cfg* cfg, const doubl
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(4 * rtk::kPddCluster);
-    lc.blockDim = dim3(256);
+    // (the four edges' W values are loaded one per thread: >= 4 (m+1) threads)
+    lc.blockDim = dim3(std::max(256, (4 * (G.m + 1) + 31) / 32 * 32));
     lc.dynamicSmemBytes = smem;
     lc.stream = st;
     cudaLaunchAttribute at[1];
@@ -1145,7 +1146,8 @@ static rt_status pdd_downstream(rt_handle* h, const rt_pdd_cfg* cfg, const doubl
   RT_CUDA(cudaFuncSetAttribute((const void*)rtk::pdd_adi_kernel,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   // the pointwise reaction spreads over many threads; the line sweeps use m-1 of them
-  const int threads = std::min(1024, std::max(256, ((G.m + 1) * (G.m + 1) / 4 + 31) / 32 * 32));
+  // (at most 512: 1024 threads x 64 registers exceed the register file)
+  const int threads = std::min(512, std::max(256, ((G.m + 1) * (G.m + 1) / 4 + 31) / 32 * 32));
   rtk::pdd_adi_kernel<<<4, threads, smem, st>>>(bc, d_field, G, pdd_eq(h->p));
   RT_CUDA(cudaGetLastError());
   return RT_OK;

@@ -33,7 +33,7 @@ CFG = dict(lo=-2.0, hi=2.0, T=0.5, n_cells=40, n_steps=100, n_s=17, n_t=6, bound
            L=5, M=5, n_trees=100_000, seed=0)
 
 
-@pytest.mark.parametrize("which", ["heat", "synthetic", "cfg3_eq"])
+@pytest.mark.parametrize("which", ["heat", "synthetic", "cfg3_eq", "cfg3_eq_large"])
 def test_pdd_downstream_parity(P, which):
     cfg = dict(CFG)
     if which == "heat":
@@ -41,6 +41,8 @@ def test_pdd_downstream_parity(P, which):
     else:
         eq = W.get("cfg3")["eq"]
         cfg.update(n_cells=64, n_steps=150, n_s=9, n_t=5, lo=-1.5, hi=2.5)
+        if which == "cfg3_eq_large":   # 79 unknowns per line: one CTA per subdomain, Thomas
+            cfg.update(n_cells=160, n_steps=60)
     nodes = PO.pdd_nodes(cfg)
     tk = cfg["T"] * np.arange(cfg["n_t"]) / (cfg["n_t"] - 1)
     if which == "heat":
@@ -149,12 +151,14 @@ def test_pdd_solve_early_levels_degenerate_table(P, orc):
     assert np.max(np.abs(F - Fo)) <= 1e-11 * max(1.0, np.max(np.abs(Fo)))
 
 
-def test_pdd_cluster_solver_equals_single_cta(P, monkeypatch):
+@pytest.mark.parametrize("n_cells", [64, 130])
+def test_pdd_cluster_solver_equals_single_cta(P, monkeypatch, n_cells):
     """The local solver spread over a thread-block cluster per subdomain
     (pdd_adi_cluster_kernel, DSMEM copies) performs every value's arithmetic
-    exactly as the single-CTA kernel: the fields agree bit for bit."""
+    exactly as the single-CTA kernel: the fields agree bit for bit (n_cells
+    = 130: 64 unknowns per line, the largest the cluster path takes)."""
     eq = W.get("cfg3")["eq"]
-    cfg = dict(CFG, n_cells=64, n_steps=150, n_s=9, n_t=5, lo=-1.5, hi=2.5)
+    cfg = dict(CFG, n_cells=n_cells, n_steps=150, n_s=9, n_t=5, lo=-1.5, hi=2.5)
     nodes = PO.pdd_nodes(cfg)
     rng = np.random.default_rng(5)
     tk = cfg["T"] * np.arange(cfg["n_t"]) / (cfg["n_t"] - 1)
