@@ -95,6 +95,7 @@ struct rt_handle {
   int64_t tpt_override = 0;
   int32_t pool_override = 0;
   bool pdd_cluster = true;   // RT_PDD_CLUSTER=0: the single-CTA local solver (A/B tests)
+  bool force_gen = false;    // RT_FORCE_GEN=1: the general tree-walk kernel everywhere (tests)
 };
 
 // ---------------------------------------------------------------------------
@@ -212,6 +213,7 @@ extern "C" rt_status rt_create(const rt_eq_params* params, rt_handle** out) {
   rt_handle* h = new rt_handle();
   h->p = p;
   if (const char* e = std::getenv("RT_PDD_CLUSTER")) h->pdd_cluster = std::atoi(e) != 0;
+  if (const char* e = std::getenv("RT_FORCE_GEN")) h->force_gen = std::atoi(e) != 0;
   h->nz = nz;
   cudaError_t e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
   for (int q = 0; q < 4 && e == cudaSuccess; ++q) e = cudaEventCreate(&h->ev[q]);
@@ -648,7 +650,7 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   for (int k = 0; k <= 8; ++k) var = var || p.coef_kind[k] != RT_COEF_CONST;
   // the general kernel only where f2/f3 weight factors, > 3 offspring kinds or
   // an empty support (purely linear f) need it
-  const bool gen = p.strategy != RT_STRATEGY_POTENTIAL || var || nz.n_support > 3 ||
+  const bool gen = h->force_gen || p.strategy != RT_STRATEGY_POTENTIAL || var || nz.n_support > 3 ||
                    nz.n_support == 0;
   KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, p.precision == RT_PREC_FP32_POS,
                            p.strategy == RT_STRATEGY_B, sh, gen, &prod, &smem, &pool_cap);

@@ -393,6 +393,22 @@ def test_host_api_equals_device_api(P):
     assert est.stats()["total_ms"] > 0
 
 
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg4", "heat_d2_tanh"])
+def test_specialised_kernel_equals_general(P, monkeypatch, name):
+    """The GEN = false tree walk (no f2/f3 weight factors, 1-3 offspring kinds)
+    performs the general kernel's arithmetic: sums and per-tree records are
+    bitwise equal (RT_FORCE_GEN=1 selects the general kernel)."""
+    eq, pts, t, N = CASES[name]
+    x = dev(pts)
+    a = P.Estimator(eq).sums(x, t, 4 * N, seed=3).cpu().numpy()
+    ra, _ = P.Estimator(eq).trace(x, t, N, seed=4)
+    monkeypatch.setenv("RT_FORCE_GEN", "1")
+    b = P.Estimator(eq).sums(x, t, 4 * N, seed=3).cpu().numpy()
+    rb, _ = P.Estimator(eq).trace(x, t, N, seed=4)
+    assert np.array_equal(a, b)
+    assert np.array_equal(ra, rb)
+
+
 def test_host_call_after_async_dev_call(P):
     """a host call (own stream) right after an unsynchronised _dev
     call on another stream shares the handle's scratch; it must wait for it.
