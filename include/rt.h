@@ -36,6 +36,11 @@
  *     seed) and the launch geometry; with a fixed geometry they are bitwise
  *     reproducible run to run, and tree j of node i is the same tree whatever
  *     range or geometry computes it (counter-based RNG).
+ *   - Diagnostic environment switches (tests only; none changes a result):
+ *     RT_FORCE_GEN=1 (read by rt_create) selects the general tree-walk kernel
+ *     where the specialised one would run; RT_PDD_CLUSTER=0 (rt_create) the
+ *     single-CTA PDD local solver; RT_WARP_TIMES=<file> appends per-warp
+ *     start/end times of every tree-walk launch to <file>.
  */
 #ifndef RT_H
 #define RT_H
