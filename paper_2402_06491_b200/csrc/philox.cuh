@@ -61,9 +61,9 @@ __device__ __forceinline__ double unif53(uint32_t lo, uint32_t hi) {
 // Uniform in (0,1) from 32 random bits: (2w+1)·2^-33, exactly, via
 // d = 1 + w·2^-32 and d − (1 − 2^-33).
 __device__ __forceinline__ double unif32(uint32_t w) {
-  const double d = __hiloint2double(static_cast<int>((w >> 12) | 0x3FF00000u),
-                                    static_cast<int>(w << 20));
-  return d - 0x1.ffffffffp-1;
+  // (2w+1)·2^-33 = w·2^-32 + 2^-33, exact (33 significant bits): one
+  // conversion (XU pipe) and one DFMA with power-of-two immediates
+  return fma(static_cast<double>(w), 0x1p-32, 0x1p-33);
 }
 
 }  // namespace rtk
