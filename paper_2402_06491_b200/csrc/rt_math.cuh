@@ -101,13 +101,13 @@ RTM_HD double log_tab(double x, const LogEntry* T) {
   const LogEntry e = T[i];
   const double r = fma_d(z, e.invc, -1.0);
   double p = kLogPTop;
-  p = fma_d(p, r, kLogP[4]);
-  p = fma_d(p, r, kLogP[3]);
-  p = fma_d(p, r, kLogP[2]);
-  p = fma_d(p, r, kLogP[1]);
-  p = fma_d(p, r, kLogP[0]);
+  p = fma_d(p, r, kLogPL[4]);
+  p = fma_d(p, r, kLogPL[3]);
+  p = fma_d(p, r, kLogPL[2]);
+  p = fma_d(p, r, kLogPL[1]);
+  p = fma_d(p, r, kLogPL[0]);
   const double r2 = r * r;
-  const double t = fma_d(static_cast<double>(k), kLn2, e.logc);
+  const double t = fma_d(static_cast<double>(k), kLogPL[5], e.logc);   // kLogPL[5] = ln2
   return t + fma_d(r2, p, r);
 }
 

@@ -536,9 +536,9 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
         y[1] = fma(rad, sn, y[1]);
       } else {
         // (e1 = 0 when the two spacing words tie — probability 2^-32: the
-        // 1e-300 keeps the root positive and changes nothing else, since it
-        // is absorbed by any 2·e1·h2d > 1e-284)
-        const double rad = sqrt_pos(fma(2.0 * e1, h2d, 1e-300));
+        // 2^-996 (≈ 1.5e-300, an FP64 immediate) keeps the root positive and
+        // changes nothing else, since it is absorbed by any 2·e1·h2d > 1e-284)
+        const double rad = sqrt_pos(fma(2.0 * e1, h2d, 0x1p-996));
         double sn, cs;
         sincos2pi_u32(r0.w, sn, cs);
         y[0] = fma(rad, cs, y[0]);
