@@ -281,6 +281,10 @@ static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, bool sb, bool sh
       *prod = pick_kernel<D, G, false, false, false, true>();                   \
       return rec ? pick_kernel<D, G, true, false, false, true>() : *prod;       \
     }                                                                           \
+    if (sb && !gen) {                                                           \
+      *prod = pick_kernel<D, G, false, false, true, false, false>();            \
+      return rec ? pick_kernel<D, G, true, false, true, false, false>() : *prod; \
+    }                                                                           \
     if (sb) {                                                                   \
       *prod = pick_kernel<D, G, false, false, true>();                          \
       return rec ? pick_kernel<D, G, true, false, true>() : *prod;              \
@@ -648,9 +652,10 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
   const bool sh = p.shared != 0;
   bool var = false;
   for (int k = 0; k <= 8; ++k) var = var || p.coef_kind[k] != RT_COEF_CONST;
-  // the general kernel only where f2/f3 weight factors, > 3 offspring kinds or
-  // an empty support (purely linear f) need it
-  const bool gen = h->force_gen || p.strategy != RT_STRATEGY_POTENTIAL || var || nz.n_support > 3 ||
+  // the general kernel only where f2 weight factors (the shift, variable
+  // coefficients), > 3 offspring kinds or an empty support (purely linear f)
+  // need it — Strategy B with constant coefficients has none of them
+  const bool gen = h->force_gen || p.strategy == RT_STRATEGY_A_SHIFT || var || nz.n_support > 3 ||
                    nz.n_support == 0;
   KernelFn fn = kernel_for(p.dim, p.init_kind, d_recs != nullptr, p.precision == RT_PREC_FP32_POS,
                            p.strategy == RT_STRATEGY_B, sh, gen, &prod, &smem, &pool_cap);

@@ -393,7 +393,7 @@ def test_host_api_equals_device_api(P):
     assert est.stats()["total_ms"] > 0
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg4", "heat_d2_tanh"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg4", "heat_d2_tanh", "B_cfg2_k1", "ex2_B"])
 def test_specialised_kernel_equals_general(P, monkeypatch, name):
     """The GEN = false tree walk (no f2/f3 weight factors, 1-3 offspring kinds)
     performs the general kernel's arithmetic: sums and per-tree records are
