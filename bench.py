@@ -216,7 +216,8 @@ def oracle_sample(cfg: dict, budget_s: float):
     _, st = oracle.sums(eq, pts[:1], t, 2000, seed=cfg["seed"])
     per_tree = (time.perf_counter() - t0) / 2000
     n_nodes = min(len(pts), 16)
-    n_trees = max(64, int(budget_s / per_tree / n_nodes))
+    # (a subset of the workload: never more trees per node than it has)
+    n_trees = min(cfg["n_trees"], max(64, int(budget_s / per_tree / n_nodes)))
     t0 = time.perf_counter()
     _, st = oracle.sums(eq, pts[:n_nodes], t, n_trees, seed=cfg["seed"])
     dt = time.perf_counter() - t0
@@ -245,7 +246,7 @@ def oracle_sample_all_cores(cfg: dict, budget_s: float):
     t0 = time.perf_counter()
     oracle.sums(eq, pts[:1], t, 2000, seed=cfg["seed"])
     per_tree = (time.perf_counter() - t0) / 2000
-    n_trees = max(64, int(budget_s / per_tree))
+    n_trees = min(cfg["n_trees"], max(64, int(budget_s / per_tree)))
     jobs = [(eq, pts[i % len(pts):i % len(pts) + 1], t, n_trees, cfg["seed"]) for i in range(cores)]
     with mp.get_context("spawn").Pool(cores) as pool:
         pool.map(_oracle_worker, [(eq, pts[:1], t, 64, cfg["seed"])] * cores)   # start-up, oracle load

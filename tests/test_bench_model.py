@@ -78,3 +78,27 @@ def test_clock_summary_from_nvidia_smi_rows():
     c2.nvml = [(1965, 0), (1965, 0x40), (1950, 0)]
     s2 = c2.summary()
     assert s2["sm_mhz"] == 1965.0 and s2["reasons"] == ["hw_thermal_slowdown"] and s2["source"].startswith("nvml")
+
+
+def test_reference_arm_json_line():
+    """`bench.py --impl reference` (the oracle on host cores, no GPU): one JSON
+    line with the contract's keys, e2e with zero copies, and a sample that is a
+    subset of the workload (cfg1: 16 nodes x 1e4 trees, run whole)."""
+    import json
+    import subprocess
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--config", "cfg1", "--steps", "1", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["unit"] == "trees/s" and line["value"] > 0
+    assert line["config"]["workload"] == "cfg1"
+    assert line["e2e"] == {"value": line["value"], "unit": "trees/s",
+                           "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] == 1 and cb["value"] == line["value"]
+    assert cb["sample"].startswith("16 nodes x 10000 trees of cfg1")
