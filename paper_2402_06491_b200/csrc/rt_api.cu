@@ -90,7 +90,7 @@ struct rt_handle {
   bool have_timing = false;
   bool scratch_used = false;   // ev[2] marks the last use of the scratch on last_stream
   double host_total_ms = -1.0;
-  DevBuf partials, gpool, gaux, lacc, wtime, sh_tsum, sh_leaves, sh_sorted, sh_boff, pdd_pts, pdd_nodal, pdd_bc, pdd_field, pdd_c, pdd_u, pdd_spl, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
+  DevBuf partials, segs, gpool, gaux, lacc, wtime, sh_tsum, sh_leaves, sh_sorted, sh_boff, pdd_pts, pdd_nodal, pdd_bc, pdd_field, pdd_c, pdd_u, pdd_spl, sums, stats, h_points, h_coeffs, h_stderr, h_aux, h_flags;
   int32_t grid_override = 0;
   int64_t tpt_override = 0;
   int32_t pool_override = 0;
@@ -230,7 +230,7 @@ extern "C" rt_status rt_destroy(rt_handle* h) {
   if (!h) return RT_OK;
   if (h->own_stream) cudaStreamSynchronize(h->own_stream);
   if (h->last_stream) cudaStreamSynchronize(h->last_stream);
-  for (DevBuf* b : {&h->partials, &h->gpool, &h->gaux, &h->lacc, &h->wtime, &h->sh_tsum, &h->sh_leaves, &h->sh_sorted, &h->sh_boff, &h->pdd_pts, &h->pdd_nodal,
+  for (DevBuf* b : {&h->partials, &h->segs, &h->gpool, &h->gaux, &h->lacc, &h->wtime, &h->sh_tsum, &h->sh_leaves, &h->sh_sorted, &h->sh_boff, &h->pdd_pts, &h->pdd_nodal,
                     &h->pdd_bc, &h->pdd_field, &h->pdd_c, &h->pdd_u, &h->pdd_spl, &h->sums, &h->stats, &h->h_points, &h->h_coeffs,
                     &h->h_stderr, &h->h_aux, &h->h_flags})
     b->release();
@@ -360,23 +360,51 @@ static rt_status plan_launch(rt_handle* h, KernelFn fn, int smem, int64_t n_poin
 }
 
 constexpr int kReduceWarps = 8;
+constexpr int64_t kReduceSeg = 512;   // tasks per segment (at least; see reduce_seg)
+
+// Tasks per segment of the second pass: a function of the task count alone
+// (never of the GPU), so the summation order — and the sums' bits — are fixed
+// by the launch's task decomposition.
+static inline int64_t reduce_seg(int64_t tpn) {
+  return std::max<int64_t>(kReduceSeg, (tpn + 65534) / 65535);
+}
+
+// Adds (bin counts → trees, pruned trees, splits) of one node's finished sums
+// to the event counters; lane = bin, all 32 lanes
+__device__ __forceinline__ void fold_bin_counts(int b, int nb, double c, unsigned long long* stats) {
+  unsigned long long trees = b < nb ? static_cast<unsigned long long>(c) : 0ull;
+  unsigned long long splits = trees * static_cast<unsigned long long>(b);
+  for (int o = 16; o > 0; o >>= 1) {
+    trees += __shfl_xor_sync(0xffffffffu, trees, o);
+    splits += __shfl_xor_sync(0xffffffffu, splits, o);
+  }
+  if (b == 0) {
+    atomicAdd(stats + 0, trees);
+    atomicAdd(stats + 4, splits);
+  }
+  if (b == nb - 1) atomicAdd(stats + 1, static_cast<unsigned long long>(c));
+}
 
 __global__ void __launch_bounds__(32 * kReduceWarps)
-reduce_tasks_kernel(const double* __restrict__ partials, int64_t tpn, int nb,
-                    double* __restrict__ sums, unsigned long long* __restrict__ stats) {
-  // second pass, atomic-free and deterministic: node i's tasks are summed by
-  // eight warps — warp w takes tasks w, w+8, w+16, … in ascending order, lane
-  // = bin — and the eight partial sums are added in warp order; the exact bin
-  // counts also give trees, pruned trees and splits (a pruned tree aborted at
-  // its (K+1)-th split)
+reduce_tasks_kernel(const double* __restrict__ partials, int64_t tpn, int nb, int64_t seg,
+                    double* __restrict__ out, unsigned long long* __restrict__ stats) {
+  // second pass, atomic-free and deterministic: CTA (i, s) sums node i's
+  // tasks [s·seg, (s+1)·seg) with eight warps — warp w takes the segment's
+  // tasks w, w+8, w+16, … in ascending order, lane = bin — and adds the eight
+  // partial sums in warp order.  One segment: the node's sums, and the exact
+  // bin counts also give trees, pruned trees and splits (a pruned tree
+  // aborted at its (K+1)-th split).  Several: per-segment sums, combined in
+  // segment order by reduce_segments_kernel (the segments give a node with
+  // many tasks — shared trees, few nodes — enough CTAs to stream its partials).
   __shared__ double part[kReduceWarps][32][3];
-  const int64_t i = blockIdx.x;
+  const int64_t i = blockIdx.x, sg = blockIdx.y, nseg = gridDim.y;
   const int b = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t q0 = sg * seg, q1 = min(tpn, q0 + seg);
   double s1 = 0.0, s2 = 0.0, c = 0.0;
   if (b < nb) {
     const int64_t st = static_cast<int64_t>(nb) * 3;
-    const double* p = partials + (i * tpn * nb + b) * 3 + w * st;
-    for (int64_t q = w; q < tpn; q += kReduceWarps, p += kReduceWarps * st) {
+    const double* p = partials + (i * tpn * nb + b) * 3 + (q0 + w) * st;
+    for (int64_t q = q0 + w; q < q1; q += kReduceWarps, p += kReduceWarps * st) {
       s1 += p[0];
       s2 += p[1];
       c += p[2];
@@ -395,22 +423,56 @@ reduce_tasks_kernel(const double* __restrict__ partials, int64_t tpn, int nb,
     c += part[v][b][2];
   }
   if (b < nb) {
+    double* o = out + ((i * nseg + sg) * nb + b) * 3;
+    o[0] = s1;
+    o[1] = s2;
+    o[2] = c;
+  }
+  if (nseg == 1) fold_bin_counts(b, nb, c, stats);
+}
+
+// Node i's segment sums added in segment order (one warp per node, lane = bin).
+__global__ void __launch_bounds__(32)
+reduce_segments_kernel(const double* __restrict__ segs, int64_t nseg, int nb,
+                       double* __restrict__ sums, unsigned long long* __restrict__ stats) {
+  const int64_t i = blockIdx.x;
+  const int b = threadIdx.x;
+  double s1 = 0.0, s2 = 0.0, c = 0.0;
+  if (b < nb) {
+    const double* p = segs + (i * nseg * nb + b) * 3;
+    for (int64_t sg = 0; sg < nseg; ++sg, p += static_cast<int64_t>(nb) * 3) {
+      s1 += p[0];
+      s2 += p[1];
+      c += p[2];
+    }
     double* o = sums + (i * nb + b) * 3;
     o[0] = s1;
     o[1] = s2;
     o[2] = c;
   }
-  unsigned long long trees = b < nb ? static_cast<unsigned long long>(c) : 0ull;
-  unsigned long long splits = trees * static_cast<unsigned long long>(b);
-  for (int o = 16; o > 0; o >>= 1) {
-    trees += __shfl_xor_sync(0xffffffffu, trees, o);
-    splits += __shfl_xor_sync(0xffffffffu, splits, o);
+  fold_bin_counts(b, nb, c, stats);
+}
+
+// The second pass over partials[n_points][tpn][nb][3] into d_sums[n_points][nb][3].
+static rt_status launch_reduce(rt_handle* h, int64_t n_points, int64_t tpn, int nb, double* d_sums,
+                               cudaStream_t st) {
+  const int64_t seg = reduce_seg(tpn), nseg = (tpn + seg - 1) / seg;
+  auto* stats = static_cast<unsigned long long*>(h->stats.p);
+  const auto* parts = static_cast<const double*>(h->partials.p);
+  if (nseg <= 1) {
+    reduce_tasks_kernel<<<dim3(static_cast<unsigned>(n_points), 1), 32 * kReduceWarps, 0, st>>>(
+        parts, tpn, nb, seg, d_sums, stats);
+    RT_CUDA(cudaGetLastError());
+    return RT_OK;
   }
-  if (b == 0) {
-    atomicAdd(stats + 0, trees);
-    atomicAdd(stats + 4, splits);
-  }
-  if (b == nb - 1) atomicAdd(stats + 1, static_cast<unsigned long long>(c));
+  RT_CUDA(h->segs.ensure(static_cast<size_t>(n_points) * nseg * nb * 3 * sizeof(double)));
+  auto* segs = static_cast<double*>(h->segs.p);
+  reduce_tasks_kernel<<<dim3(static_cast<unsigned>(n_points), static_cast<unsigned>(nseg)),
+                        32 * kReduceWarps, 0, st>>>(parts, tpn, nb, seg, segs, stats);
+  RT_CUDA(cudaGetLastError());
+  reduce_segments_kernel<<<static_cast<unsigned>(n_points), 32, 0, st>>>(segs, nseg, nb, d_sums, stats);
+  RT_CUDA(cudaGetLastError());
+  return RT_OK;
 }
 
 __global__ void finalize_kernel(const double* __restrict__ sums, int K, double N,
@@ -628,10 +690,10 @@ static rt_status run_walk_shared(rt_handle* h, KernelFn prod, int smem, int pool
     q0 += eg.y;
   }
   RT_CUDA(cudaEventRecord(h->ev[1], st));
-  reduce_tasks_kernel<<<static_cast<unsigned>(n_points), 32 * kReduceWarps, 0, st>>>(
-      static_cast<double*>(h->partials.p), tpn_total, nb, d_sums,
-      static_cast<unsigned long long*>(h->stats.p));
-  RT_CUDA(cudaGetLastError());
+  {
+    const rt_status o = launch_reduce(h, n_points, tpn_total, nb, d_sums, st);
+    if (o != RT_OK) return o;
+  }
   mark_scratch(h, st);
   h->have_timing = true;
   h->host_total_ms = -1.0;
@@ -726,10 +788,10 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
     }
   }
   RT_CUDA(cudaEventRecord(h->ev[1], st));
-  reduce_tasks_kernel<<<static_cast<unsigned>(n_points), 32 * kReduceWarps, 0, st>>>(
-      static_cast<double*>(h->partials.p), L.tpn, nb, d_sums,
-      static_cast<unsigned long long*>(h->stats.p));
-  RT_CUDA(cudaGetLastError());
+  {
+    const rt_status o = launch_reduce(h, n_points, L.tpn, nb, d_sums, st);
+    if (o != RT_OK) return o;
+  }
   mark_scratch(h, st);
   h->have_timing = true;
   h->host_total_ms = -1.0;

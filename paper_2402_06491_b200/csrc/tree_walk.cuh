@@ -776,6 +776,23 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
         __syncwarp();
         if (done) start_tree(iss_next + static_cast<uint32_t>(rank));
         iss_next += static_cast<uint32_t>(nfin);
+      } else if constexpr (SH) {
+        // shared trees: a task carries no sums of its own (phase 1 stores
+        // per-tree summaries), so lanes need no clean start — the lanes the
+        // task cannot serve take the next task's trees at once instead of
+        // idling until the task's longest tree ends
+        __syncwarp();
+        if (done && static_cast<uint32_t>(rank) < avail) start_tree(iss_next + static_cast<uint32_t>(rank));
+        iss_next += avail;
+        const uint32_t need = static_cast<uint32_t>(nfin) - avail;
+        next_task();                                       // (warp-uniform)
+        const uint32_t got = stream_end ? 0u : min(need, iss_end - iss_next);
+        if (done && static_cast<uint32_t>(rank) >= avail) {
+          const uint32_t r2 = static_cast<uint32_t>(rank) - avail;
+          if (r2 < got) start_tree(iss_next + r2);
+          else active = false;
+        }
+        iss_next += got;
       } else {                                             // the task's trees run out
         __syncwarp();
         if (done) {
@@ -786,6 +803,12 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
         if (left == 0) close_and_next();                   // every tree recorded
       }
     }
+  }
+  if constexpr (SH) {                 // (streamed tasks: the leaf count is folded once)
+    unsigned long long v1 = static_cast<unsigned long long>(c_leaf) * static_cast<unsigned long long>(P.n_points);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+    if (lane == 0) atomicAdd(P.stats + 3, v1);
   }
   if (P.wtime != nullptr && lane == 0) {
     unsigned smid;
