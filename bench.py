@@ -101,9 +101,22 @@ def algo_fp64_ops(eq: dict, stats: dict, n_points: int = 1, basis: str = "contra
     Shared trees (f4): the statistics count per (node, tree), but the method
     walks each tree once for all n_points nodes — particles and splits are
     credited once per tree; the g evaluations (leaves) and the per-tree
-    accumulation happen per node."""
+    accumulation happen per node (Gaussian data: one exponential per (node,
+    tree), the leaves' moments once per tree)."""
     u = algo_fp64_per_unit(eq, basis)
     walk = 1.0 / n_points if eq.get("shared") else 1.0
+    if eq.get("shared") and eq["init_kind"] == W.G_GAUSS:
+        # Gaussian data (DESIGN.md §12): the leaf product is W amp^L
+        # e^{-(L|x+μ|² + V)/s²} — per leaf, once per tree: Σδ (d), Σ|δ|² (d + 1),
+        # Π *= amp (1); per tree once: μ (reciprocal + d), V (d); per (node,
+        # tree): x + μ (d), |·|² (d), L·q + V, /s², exp, W × (3)
+        d = eq["dim"]
+        per_leaf = 2 * d + 2 + (1 if eq.get("strategy", 0) == 2 else 0)
+        per_tree_once = SV["div"] + 2 * d
+        per_node_tree = 2 * d + 3 + SV["exp"]
+        return (stats["particles"] * walk * u["particle"] + stats["leaves"] * walk * per_leaf +
+                stats["splits"] * walk * u["split"] + stats["trees"] * walk * per_tree_once +
+                stats["trees"] * (per_node_tree + u["tree"]))
     return (stats["particles"] * walk * u["particle"] + stats["leaves"] * u["leaf"] +
             stats["splits"] * walk * u["split"] + stats["trees"] * u["tree"])
 

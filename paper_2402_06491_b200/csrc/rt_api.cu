@@ -599,7 +599,9 @@ static rt_status run_walk_shared(rt_handle* h, KernelFn prod, int smem, int pool
   int kmax = 0;
   for (int q = 0; q < nz.n_support; ++q) kmax = std::max(kmax, nz.support[q]);
   const int lmax = 1 + p.K * std::max(0, kmax - 1);           // leaves of a kept tree
-  const double per_tree = static_cast<double>(lmax) * d * 8 + sizeof(rtk::TreeSum);
+  // per-tree slot: the leaf displacements, or μ and V for Gaussian data
+  const int64_t slot = p.init_kind == RT_G_GAUSS ? d + 1 : static_cast<int64_t>(lmax) * d;
+  const double per_tree = static_cast<double>(slot) * 8 + sizeof(rtk::TreeSum);
   int64_t M = std::max<int64_t>(1, std::min<int64_t>(n_trees, static_cast<int64_t>(4.0e9 / per_tree)));
   if (h->tpt_override > 0) M = std::min(M, h->tpt_override);   // (tests: force several chunks)
   const int64_t n_chunks = (n_trees + M - 1) / M;
@@ -625,7 +627,7 @@ static rt_status run_walk_shared(rt_handle* h, KernelFn prod, int smem, int pool
   for (int64_t c = 0; c < n_chunks; ++c) tpn_total += (std::min(M, n_trees - c * M) + tpb - 1) / tpb;
   RT_CUDA(h->partials.ensure(static_cast<size_t>(n_points) * tpn_total * nb * 3 * sizeof(double)));
   RT_CUDA(h->sh_tsum.ensure(static_cast<size_t>(M) * sizeof(rtk::TreeSum)));
-  RT_CUDA(h->sh_leaves.ensure(static_cast<size_t>(M) * lmax * d * sizeof(double)));
+  RT_CUDA(h->sh_leaves.ensure(static_cast<size_t>(M) * slot * sizeof(double)));
   RT_CUDA(h->sh_sorted.ensure(static_cast<size_t>(M) * sizeof(rtk::TreeSum)));
   RT_CUDA(h->sh_boff.ensure(static_cast<size_t>((M + tpb - 1) / tpb) * (nb + 1) * sizeof(int32_t)));
   const int gcap = 32 * (p.K + 1);

@@ -11,7 +11,12 @@
 // accumulated per order bin (ΣC, ΣC²; counts are node-free) in registers,
 // one bin run at a time.  Results per (node, tree block) go to the per-node
 // task partials that the shared task reduction sums in block order
-// (deterministic).
+// (deterministic).  Gaussian g: phase 1 stored each tree's leaf mean μ and
+// scatter V instead of its leaves, and C_i = W amp^L e^{−(L|x_i+μ|² + V)/s²}
+// is ONE exponential per (node, tree) whatever the leaf count (the identity
+// Σ_l |x+δ_l|² = L|x+μ|² + Σ_l |δ_l−μ|²; both terms ≥ 0, so no cancellation
+// against the node position); the CTA stages 64 trees' (W, L, μ, V) in
+// shared memory at a time.
 #pragma once
 #include <cstdint>
 
@@ -113,7 +118,30 @@ shared_eval_kernel(const __grid_constant__ EvalParams E) {
   const int64_t j1 = min(E.M, j0 + E.tpb);
 
   // C_i = W Π_l g(x_i + δ_l) of tree ts (leaf slots of chunk tree jl)
+  // Gaussian g: W amp^L e^{−(L|x+μ|² + V)/s²} (W carries amp^L; μ, V from
+  // phase 1) — both terms non-negative, so the exponent is accurate to a few
+  // ulps of itself wherever the node lies
+  auto gauss_prod = [&](double W, int nl, const double (&m)[DIM + 1], double (&prod)[kNpt]) {
+    const double V = m[DIM], L = static_cast<double>(nl);
+#pragma unroll
+    for (int a = 0; a < kNpt; ++a) {
+      double q = 0.0;
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) {
+        const double z = x[a][k] + m[k];
+        q = fma(z, z, q);
+      }
+      prod[a] = W * exp_neg(-(fma(L, q, V) * E.inv_scale2));
+    }
+  };
   auto tree_prod = [&](const TreeSum& ts, int64_t jl, double (&prod)[kNpt]) {
+    if constexpr (sh_moments<GK>()) {
+      double m[DIM + 1];
+#pragma unroll
+      for (int k = 0; k <= DIM; ++k) m[k] = E.leaves[jl * (DIM + 1) + k];
+      gauss_prod(ts.W, ts.nl, m, prod);
+      return;
+    }
 #pragma unroll
     for (int a = 0; a < kNpt; ++a) prod[a] = ts.W;
     const double* lf = E.leaves + jl * E.lmax * DIM;
@@ -163,31 +191,83 @@ shared_eval_kernel(const __grid_constant__ EvalParams E) {
     for (int a = 0; a < kNpt; ++a)
       ob[a] = (static_cast<int64_t>(valid[a] ? node[a] : 0) * E.tpn_total + E.q0 + blockIdx.y) * E.nb * 3;
     const int n_kept = bo[E.K + 1];                  // runs of bins 0..K, then the pruned run
-    TreeSum nxt;
-    if (n_kept > 0) nxt = srt[0];
-    int r = 0;
-    for (int b = 0; b <= E.K; ++b) {
-      const int r1 = bo[b + 1];
+    if constexpr (sh_moments<GK>()) {
+      // Gaussian g: the CTA stages 64 trees' (W, L, μ, V) in shared memory at
+      // a time — one coalesced gather by all threads instead of a dependent
+      // global load per tree per warp — then every thread walks them in order
+      __shared__ double sW[kEvalThreads], sM[DIM + 1][kEvalThreads];
+      __shared__ int sL[kEvalThreads];
       double s1[kNpt], s2[kNpt];
 #pragma unroll
       for (int a = 0; a < kNpt; ++a) { s1[a] = 0.0; s2[a] = 0.0; }
-      for (; r < r1; ++r) {
-        const TreeSum ts = nxt;
-        if (r + 1 < n_kept) nxt = srt[r + 1];        // warp-uniform, prefetched
-        double prod[kNpt];
-        tree_prod(ts, ts.parts, prod);
+      int b = 0, bend = bo[1];
+      auto flush = [&]() {                           // bin b's run is complete
+        const double cnt = static_cast<double>(bo[b + 1] - bo[b]);
 #pragma unroll
         for (int a = 0; a < kNpt; ++a) {
-          s1[a] += prod[a];
-          s2[a] = fma(prod[a], prod[a], s2[a]);
+          if (valid[a]) {
+            double* o = E.partials + ob[a] + b * 3;
+            o[0] = s1[a]; o[1] = s2[a]; o[2] = cnt;
+          }
+          s1[a] = 0.0; s2[a] = 0.0;
+        }
+        ++b;
+        bend = bo[b + 1];
+      };
+      for (int r0 = 0; r0 < n_kept; r0 += kEvalThreads) {   // (CTA-uniform bounds)
+        const int nt = min(kEvalThreads, n_kept - r0);
+        __syncthreads();
+        if (tid < nt) {
+          const TreeSum ts = srt[r0 + tid];
+          sW[tid] = ts.W;
+          sL[tid] = ts.nl;
+          const double* m = E.leaves + static_cast<int64_t>(ts.parts) * (DIM + 1);
+#pragma unroll
+          for (int k = 0; k <= DIM; ++k) sM[k][tid] = m[k];
+        }
+        __syncthreads();
+        for (int u = 0; u < nt; ++u) {
+          while (r0 + u >= bend) flush();
+          double m[DIM + 1];
+#pragma unroll
+          for (int k = 0; k <= DIM; ++k) m[k] = sM[k][u];
+          double prod[kNpt];
+          gauss_prod(sW[u], sL[u], m, prod);
+#pragma unroll
+          for (int a = 0; a < kNpt; ++a) {
+            s1[a] += prod[a];
+            s2[a] = fma(prod[a], prod[a], s2[a]);
+          }
         }
       }
-      const double cnt = static_cast<double>(r1 - bo[b]);
+      while (b <= E.K) flush();                      // the last run and the empty bins after it
+    } else {
+      TreeSum nxt;
+      if (n_kept > 0) nxt = srt[0];
+      int r = 0;
+      for (int b = 0; b <= E.K; ++b) {
+        const int r1 = bo[b + 1];
+        double s1[kNpt], s2[kNpt];
 #pragma unroll
-      for (int a = 0; a < kNpt; ++a) {
-        if (valid[a]) {
-          double* o = E.partials + ob[a] + b * 3;
-          o[0] = s1[a]; o[1] = s2[a]; o[2] = cnt;
+        for (int a = 0; a < kNpt; ++a) { s1[a] = 0.0; s2[a] = 0.0; }
+        for (; r < r1; ++r) {
+          const TreeSum ts = nxt;
+          if (r + 1 < n_kept) nxt = srt[r + 1];        // warp-uniform, prefetched
+          double prod[kNpt];
+          tree_prod(ts, ts.parts, prod);
+#pragma unroll
+          for (int a = 0; a < kNpt; ++a) {
+            s1[a] += prod[a];
+            s2[a] = fma(prod[a], prod[a], s2[a]);
+          }
+        }
+        const double cnt = static_cast<double>(r1 - bo[b]);
+#pragma unroll
+        for (int a = 0; a < kNpt; ++a) {
+          if (valid[a]) {
+            double* o = E.partials + ob[a] + b * 3;
+            o[0] = s1[a]; o[1] = s2[a]; o[2] = cnt;
+          }
         }
       }
     }

@@ -64,6 +64,12 @@ constexpr int kWarpsPerCta = 4;
 constexpr int kThreads = 32 * kWarpsPerCta;
 constexpr uint64_t kLabelMask = (1ull << 56) - 1;
 
+// Shared trees with Gaussian data (GK = 2) store per tree, instead of its
+// leaf displacements, their mean μ and scatter V = Σ_l |δ_l − μ|² (DIM + 1
+// doubles): Π_l amp e^{−|x+δ_l|²/s²} = amp^L e^{−(L|x+μ|² + V)/s²}, one
+// exponential per (node, tree) in phase 2.
+template <int GK> __host__ __device__ constexpr bool sh_moments() { return GK == 2; }
+
 // Stack-pool entries per warp in shared memory (<= 255: 8-bit free list) and
 // resident CTAs per SM.  Sized from the warp's depth-sum distribution (see
 // the header) and the 228 KB of shared memory / 64 K registers per SM.  The
@@ -124,6 +130,7 @@ struct WalkParams {
   int32_t n_points;            // nodes (shared trees: the stats are per (node, tree))
   // shared trees (f4), phase 1: per-tree summaries and leaf displacements of
   // trees [tree_offset, tree_offset + n_trees): tsum[j], leaves[j][lmax][DIM]
+  // (Gaussian g: leaves[j][DIM + 1] = μ, V — see sh_moments)
   struct TreeSum* tsum;
   double* leaves;
   int32_t lmax;
@@ -352,6 +359,9 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   int ne = 0, top = -1;                // top: the lane's top stack entry (-1: empty)
   int leaves = 0, parts = 0;           // per-tree counts (trace variant only)
   int c_leaf = 0;                      // leaves since the last task close
+  double m1[DIM], m2 = 0.0;            // SH, Gaussian g: Σ δ_l and Σ |δ_l|² of the tree's leaves
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) m1[k] = 0.0;
 
   auto start_tree = [&](uint32_t j) {  // a fresh tree j of the current task
     tj = j;
@@ -359,6 +369,11 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     for (int k = 0; k < DIM; ++k) y[k] = SH ? PT(0) : static_cast<PT>(ws->iss_y[k]);   // SH: δ = 0
     tau = P.t; label = 1; Pi = GEN ? P.root : 1.0; ne = 0; top = -1;   // (GEN = false: no shift, root factor 1)
     if constexpr (REC || SH) { leaves = 0; parts = 0; }
+    if constexpr (SH && sh_moments<GK>()) {
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) m1[k] = 0.0;
+      m2 = 0.0;
+    }
     active = true;
   };
 
@@ -592,7 +607,8 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const bool dead = split && (ne > P.K || (GEN && P.n_support == 0));   // (GEN = false: support non-empty)
     const bool branch = split && !dead;
     // g at a leaf; h^(α) = c'_α at a split
-    const double gl = SH ? 1.0 : gv;            // SH: g is applied per node below
+    // SH: g is applied per node in phase 2 (Gaussian: its amplitude here)
+    const double gl = SH ? (sh_moments<GK>() ? P.amp : 1.0) : gv;
     // (a killed tree's wk is 0 — entry 0 of an empty support; a pruned tree
     // keeps a nonzero product, routed to the pruned bin whose sums are
     // discarded at task close)
@@ -618,11 +634,22 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     // (before the pops overwrite y): leaves[j][l] = δ of the tree's l-th leaf
     if constexpr (SH) {
       if (active && leaf) {
-        RT_CHECK(leaves < P.lmax && tj - static_cast<uint32_t>(P.tree_offset) < static_cast<uint32_t>(P.n_trees));
-        double* const o = P.leaves + (static_cast<int64_t>(tj - static_cast<uint32_t>(P.tree_offset)) *
-                                          P.lmax + leaves) * DIM;
+        if constexpr (sh_moments<GK>()) {
+          double r2 = 0.0;
 #pragma unroll
-        for (int k = 0; k < DIM; ++k) o[k] = static_cast<double>(y[k]);
+          for (int k = 0; k < DIM; ++k) {
+            const double yk = static_cast<double>(y[k]);
+            m1[k] += yk;
+            r2 = fma(yk, yk, r2);
+          }
+          m2 += r2;
+        } else {
+          RT_CHECK(leaves < P.lmax && tj - static_cast<uint32_t>(P.tree_offset) < static_cast<uint32_t>(P.n_trees));
+          double* const o = P.leaves + (static_cast<int64_t>(tj - static_cast<uint32_t>(P.tree_offset)) *
+                                            P.lmax + leaves) * DIM;
+#pragma unroll
+          for (int k = 0; k < DIM; ++k) o[k] = static_cast<double>(y[k]);
+        }
         ++leaves;
       }
     }
@@ -760,6 +787,20 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
           ts.W = pruned ? 0.0 : Pi;
           RT_CHECK(tj - static_cast<uint32_t>(P.tree_offset) < static_cast<uint32_t>(P.n_trees));
           P.tsum[tj - static_cast<uint32_t>(P.tree_offset)] = ts;
+          if constexpr (sh_moments<GK>()) {
+            // μ = Σδ/L, V = Σ|δ|² − Σδ·μ (≥ 0; its rounding is O(ε Σ|δ|²),
+            // node-free — no cancellation against the node position)
+            double* const o = P.leaves + static_cast<int64_t>(tj - static_cast<uint32_t>(P.tree_offset)) * (DIM + 1);
+            const double il = leaves > 0 ? 1.0 / static_cast<double>(leaves) : 0.0;
+            double v = m2;
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) {
+              const double mu = m1[k] * il;
+              o[k] = mu;
+              v = fma(-m1[k], mu, v);
+            }
+            o[DIM] = fmax(v, 0.0);
+          }
         }
       } else {
         if (done) {                                 // bin ne (= K+1, the pruned bin, iff pruned)

@@ -45,6 +45,13 @@ def test_shared_trees_credit_the_walk_once():
     got = bench.algo_fp64_ops(eq, st, n)
     want = (1000 / n) * u["particle"] + 600 * u["leaf"] + (300 / n) * u["split"] + 100 * u["tree"]
     assert abs(got - want) < 1e-9 * want
+    # Gaussian data: one exponential per (node, tree); leaves' moments once per tree
+    eg = dict(W.get("cfg3")["eq"], shared=1)
+    ug = bench.algo_fp64_per_unit(eg)
+    got = bench.algo_fp64_ops(eg, st, n)
+    want = ((1000 / n) * ug["particle"] + (600 / n) * (2 * 2 + 2) + (300 / n) * ug["split"]
+            + (100 / n) * (8 + 2 * 2) + 100 * (2 * 2 + 3 + 15 + ug["tree"]))
+    assert abs(got - want) < 1e-9 * want
     # independent trees: no scaling whatever n_points says
     eq0 = W.get("cfg4")["eq"]
     assert bench.algo_fp64_ops(eq0, st, n) == bench.algo_fp64_ops(eq0, st)

@@ -214,6 +214,13 @@ def _eq_variants():
                               strategy=W.STRAT_A_SHIFT, lam=1.3, shared=1), W.random_nodes(35, 3, 17), 0.8, 500),
         "sh_d2_tanh": (dict(W.get("cfg3")["eq"], init_kind=W.G_TANH_STEP, init_amp=1.0, shared=1),
                        W.random_nodes(33, 2, 18), 0.5, 800),
+        # Gaussian data: phase 2 evaluates W amp^L e^{-(L|x+mu|^2 + V)/s^2} from the
+        # leaves' mean and scatter — d = 2 over two ragged
+        # tiles, and d = 3 with a negative |g| > 1 amplitude (amp^L alternates)
+        # at nodes up to |x_k| = 3 s
+        "sh_cfg3": (dict(W.get("cfg3")["eq"], shared=1), W.random_nodes(70, 2, 19), 0.5, 800),
+        "sh_d3_gauss_neg": (W._eq(3, (0.0, -0.5, -0.4, 0.3), W.G_GAUSS, -1.7, 1.5, K=10, shared=1),
+                            W.random_nodes(300, 3, 20, lo=-4.5, hi=4.5), 0.8, 300),
     }
 
 
@@ -241,7 +248,7 @@ def test_tree_parity(P, orc, name):
 
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg2_uniform", "poisson_k1",
-                                  "shift_ex5_d2", "B_ex3", "B_d3_var", "sh_cfg2", "sh_d3_shift",
+                                  "shift_ex5_d2", "B_ex3", "B_d3_var", "sh_cfg2", "sh_d3_shift", "sh_cfg3",
                                   "ex2_shift", "neg_cfg2_t2", "neg_big_d3"])
 def test_estimate_parity(P, orc, name):
     eq, pts, t, N = CASES[name]
