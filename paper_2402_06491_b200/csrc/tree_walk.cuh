@@ -30,7 +30,7 @@
 // order, so the sums are deterministic.  When all trees of a task are
 // recorded, every lane reads back and clears its words (L2 loads) and the
 // warp adds the 32 lanes' sums of each bin in a fixed butterfly order into
-// partials[task][bin]; a second kernel sums each node's tasks in task order.
+// partials[task][bin]; a second kernel sums each node's tasks in a fixed order.
 // Each task runs from a clean start (all lanes begin it together), so its
 // partials depend on the task alone: results are bitwise reproducible for a
 // fixed task size, whatever the grid or warp timing.
