@@ -285,4 +285,29 @@ RTM_HD double exp_neg(double x) {
   return x < -745.5 ? 0.0 : (p * s1) * s2;
 }
 
+// exp(x) for x <= 0 (0 below -745.5) with a 32-entry table T = kExpT32
+// (staged in shared memory by the kernel: its index is lane-divergent):
+// x = (32m + j) ln2/32 + r, |r| <= ln2/64, e^x = 2^m T_j (1 + (e^r − 1)),
+// e^r − 1 by Taylor degree 6 — 13 FP64 operations against exp_neg's 19.
+RTM_HD double exp_neg_tab(double x, const double* T) {
+  const double xc = x < -745.5 ? -745.5 : x;
+  const double kf = rint_d(xc * kExp32Inv);
+  double r = fma_d(kf, -kExp32Hi, xc);
+  r = fma_d(kf, -kExp32Lo, r);
+  double q = kExpQ[5];
+  q = fma_d(q, r, kExpQ[4]);
+  q = fma_d(q, r, kExpQ[3]);
+  q = fma_d(q, r, kExpQ[2]);
+  q = fma_d(q, r, kExpQ[1]);
+  q = fma_d(q, r, kExpQ[0]);
+  const int k = static_cast<int>(kf);
+  const double t = T[k & 31];
+  const double p = fma_d(t, q * r, t);
+  const int m = (k - (k & 31)) / 32;   // floor(k / 32), exact
+  const int m1 = m / 2, m2 = m - m1;
+  const double s1 = dfrom(static_cast<uint64_t>(1023 + m1) << 52);
+  const double s2 = dfrom(static_cast<uint64_t>(1023 + m2) << 52);
+  return x < -745.5 ? 0.0 : (p * s1) * s2;
+}
+
 }  // namespace rtk

@@ -116,6 +116,11 @@ shared_eval_kernel(const __grid_constant__ EvalParams E) {
   }
   const int64_t j0 = static_cast<int64_t>(blockIdx.y) * E.tpb;
   const int64_t j1 = min(E.M, j0 + E.tpb);
+  __shared__ double sExp[32];                  // Gaussian g: the table exp's 2^(j/32)
+  if constexpr (sh_moments<GK>()) {
+    if (tid < 32) sExp[tid] = kExpT32[tid];
+    __syncthreads();
+  }
 
   // C_i = W Π_l g(x_i + δ_l) of tree ts (leaf slots of chunk tree jl)
   // Gaussian g: W amp^L e^{−(L|x+μ|² + V)/s²} (W carries amp^L; μ, V from
@@ -131,7 +136,7 @@ shared_eval_kernel(const __grid_constant__ EvalParams E) {
         const double z = x[a][k] + m[k];
         q = fma(z, z, q);
       }
-      prod[a] = W * exp_neg(-(fma(L, q, V) * E.inv_scale2));
+      prod[a] = W * exp_neg_tab(-(fma(L, q, V) * E.inv_scale2), sExp);
     }
   };
   auto tree_prod = [&](const TreeSum& ts, int64_t jl, double (&prod)[kNpt]) {

@@ -18,6 +18,7 @@ __global__ void math_kernel(int which, const double* x, long n, double* y, doubl
     case 4: y[q] = rcp_nr(x[q]); break;
     case 6: sincos2pi_u32(static_cast<uint32_t>(x[q]), y[q], z[q]); break;
     case 7: y[q] = cos2pi_u32(static_cast<uint32_t>(x[q])); break;
+    case 8: y[q] = exp_neg_tab(x[q], kExpT32); break;
     default: y[q] = exp_neg(x[q]); break;
   }
 }

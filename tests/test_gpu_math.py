@@ -68,6 +68,8 @@ def test_device_sqrt_rcp_exp(dev):
     v, _ = _run(dev, 5, e)
     ref = np.exp(e.astype(np.longdouble))
     assert float(np.max(np.abs(v - ref) / ref)) < 4 * EPS
+    w, _ = _run(dev, 8, e)                              # the table-driven exp (shared trees)
+    assert float(np.max(np.abs(w - ref) / ref)) < 4 * EPS
 
 
 def test_device_u32_angles_bitwise(dev):

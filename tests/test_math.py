@@ -20,7 +20,7 @@ def m(tmp_path_factory):
     subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fPIC", "-shared",
                            os.path.join(HERE, "helpers", "math_host.cpp"), "-o", so])
     lib = C.CDLL(so)
-    for f in ("m_log", "m_sqrt", "m_rcp", "m_exp", "m_cospi2"):
+    for f in ("m_log", "m_sqrt", "m_rcp", "m_exp", "m_exp_tab", "m_cospi2"):
         getattr(lib, f).argtypes = [C.c_void_p, C.c_long, C.c_void_p]
     lib.m_sincospi2.argtypes = [C.c_void_p, C.c_long, C.c_void_p, C.c_void_p]
     return lib
@@ -158,3 +158,23 @@ def test_exp_neg(m):
     ref = np.exp(x.astype(np.longdouble))
     assert float(np.max(np.abs(got - ref) / ref)) < 4 * EPS
     assert _call(m, "m_exp", np.array([-800.0]))[0] == 0.0
+
+
+def test_exp_neg_tab(m):
+    """The table-driven exp (shared-tree phase 2): same bound and domain as
+    exp_neg, including every table entry's neighbourhood, the subnormal range
+    (the 2^m scaling in two exact steps) and the cut-off below -745.5."""
+    rng = np.random.default_rng(6)
+    ln2_32 = np.log(2.0) / 32
+    grid = -np.arange(0, 2000) * ln2_32
+    x = np.concatenate([-rng.exponential(3.0, 300_000), -rng.uniform(0, 708, 50_000),
+                        grid, grid - ln2_32 / 2, grid + ln2_32 / 2 - 1e-12, [0.0, -1e-300, -708.0]])
+    x = x[x <= 0]
+    got = _call(m, "m_exp_tab", x)
+    ref = np.exp(x.astype(np.longdouble))
+    assert float(np.max(np.abs(got - ref) / ref)) < 4 * EPS
+    sub = -rng.uniform(708.5, 744.0, 20_000)             # subnormal results: absolute 2^-1074 granularity
+    g2 = _call(m, "m_exp_tab", sub)
+    r2 = np.exp(sub.astype(np.longdouble))
+    assert float(np.max(np.abs(g2 - r2))) <= 2.0 ** -1074 * 2
+    assert _call(m, "m_exp_tab", np.array([-800.0]))[0] == 0.0
