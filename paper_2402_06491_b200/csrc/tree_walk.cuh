@@ -210,7 +210,7 @@ __host__ __device__ constexpr int warp_stride() {
 template <int DIM>
 __host__ __device__ constexpr int smem_bytes() {
   return 128 * 16 /* log table */ + kWarpsPerCta * ((warp_smem_bytes<DIM>() + 15) / 16 * 16) +
-         9 * 8 + 9 * 4 /* offspring weights and sizes */;
+         9 * 8 + 9 * 4 + 4 /* offspring weights and sizes */ + 32 * 8 /* exp table */;
 }
 
 // n += 1 if c, as one predicated add (ptxas otherwise emits add + select)
@@ -282,7 +282,11 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   double* const wtab = reinterpret_cast<double*>(smem_raw + 128 * 16 +
       kWarpsPerCta * wstride);                                           // [9] weights
   int* const ktab = reinterpret_cast<int*>(wtab + 9);                     // [9] offspring k
+  double* const etab = wtab + 14;                                         // [32] 2^(j/32)
   for (int q = threadIdx.x; q < 128; q += kThreads) ltab[q] = kLogTable[q];
+  if constexpr (GK == 2 && !F32) {
+    if (threadIdx.x < 32) etab[threadIdx.x] = kExpT32[threadIdx.x];
+  }
   if (threadIdx.x < 9) {
     wtab[threadIdx.x] = P.w[threadIdx.x];
     ktab[threadIdx.x] = P.kval[threadIdx.x];
@@ -578,8 +582,16 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       }
     }
     double gv;                                  // g at the leaf
-    if constexpr (F32) gv = static_cast<double>(g_eval_f<DIM, GK>(y, P));
-    else gv = g_eval<DIM, GK>(y, P);
+    if constexpr (F32) {
+      gv = static_cast<double>(g_eval_f<DIM, GK>(y, P));
+    } else if constexpr (GK == 2) {             // Gaussian: the table-driven exp
+      double r2 = y[0] * y[0];
+      if constexpr (DIM >= 2) r2 = fma(y[1], y[1], r2);
+      if constexpr (DIM >= 3) r2 = fma(y[2], y[2], r2);
+      gv = P.amp * exp_neg_tab(-r2 * P.inv_scale2, etab);
+    } else {
+      gv = g_eval<DIM, GK>(y, P);
+    }
     const int k = ktab[s];
     double wk = wtab[s];
     if constexpr (SB) wk *= tau;                // η(τ) = τ
