@@ -75,12 +75,31 @@ template <int GK> __host__ __device__ constexpr bool sh_moments() { return GK ==
 // the header) and the 228 KB of shared memory / 64 K registers per SM.  The
 // record-emitting trace variant gets one CTA less so it never spills; it is
 // launched on the production kernel's grid, so both give identical sums.
+// (RT_POOL_D<d> / RT_CTAS_D<d>: compile-time overrides for occupancy sweeps)
+#ifndef RT_POOL_D1
+#define RT_POOL_D1 192
+#endif
+#ifndef RT_POOL_D2
+#define RT_POOL_D2 176
+#endif
+#ifndef RT_POOL_D3
+#define RT_POOL_D3 144
+#endif
+#ifndef RT_CTAS_D1
+#define RT_CTAS_D1 8
+#endif
+#ifndef RT_CTAS_D2
+#define RT_CTAS_D2 8
+#endif
+#ifndef RT_CTAS_D3
+#define RT_CTAS_D3 8
+#endif
 template <int DIM> struct PoolCap;
-template <> struct PoolCap<1> { static constexpr int v = 192; };
-template <> struct PoolCap<2> { static constexpr int v = 176; };
-template <> struct PoolCap<3> { static constexpr int v = 144; };
+template <> struct PoolCap<1> { static constexpr int v = RT_POOL_D1; };
+template <> struct PoolCap<2> { static constexpr int v = RT_POOL_D2; };
+template <> struct PoolCap<3> { static constexpr int v = RT_POOL_D3; };
 template <int DIM, bool REC> struct MinCtas {
-  static constexpr int v = 8 - (REC ? 1 : 0);
+  static constexpr int v = (DIM == 1 ? RT_CTAS_D1 : DIM == 2 ? RT_CTAS_D2 : RT_CTAS_D3) - (REC ? 1 : 0);
 };
 
 struct TreeRec {   // mirrors rt_tree_rec
