@@ -49,8 +49,10 @@ N_SM, FP64_LANES, F_MAX_MHZ = 148, 64, 1965.0
 # textbook draws SURVEY §8(d) listed (a log per exponential variate and per
 # Box–Muller radius), which the kernel does not perform.  Strategy B keeps
 # the textbook Box–Muller draws (R8).  Per leaf: g (its argument, the
-# transcendental or reciprocal, the amplitude) + 1 mul; per split: 1 mul;
-# per tree: 1 mul + 2 adds.  The FP32-position variant is credited only its
+# transcendental or reciprocal, the amplitude) + 1 mul — Gaussian data on
+# independent FP64 trees: |x|², one FMA into the tree's exponent sum and the
+# amplitude per leaf, the exponential once per tree (the kernel's closed form,
+# DESIGN.md §4); per split: 1 mul; per tree: 1 mul + 2 adds.  The FP32-position variant is credited only its
 # FP64 part (clock, weights, product, sums).  basis="survey" gives SURVEY
 # §8(d)'s original textbook count (reported beside it).
 SV = dict(log=20, exp=15, sqrt=8, div=8, tanh=25, sincospi=20)
@@ -82,6 +84,13 @@ def algo_fp64_per_unit(eq: dict, basis: str = "contract") -> dict:
          W.G_LORENTZ: r2 + 1 + 1 + SV["div"] + 1}[eq["init_kind"]]   # |x|², /s², 1 +, 1/·, amp
     if f32 and basis != "survey":
         g = 0                                              # g in single precision
+    tree_g = 0
+    if eq["init_kind"] == W.G_GAUSS and not f32 and not eq.get("shared") and basis != "survey":
+        # the kernel's closed form (UseRing): a leaf adds
+        # |x|²/s² to the tree's exponent sum and multiplies amp in; the
+        # exponential is evaluated once per tree
+        g = r2 + 1 + 1                                     # |x|², fma into E, amp
+        tree_g = SV["exp"] + 1                             # exp(-E), × the tree product
     split = 1                                              # Π *= w_k
     if strat == 1:
         split += SV["exp"] + 2                             # e^{(k-1)λτ_c}
@@ -92,7 +101,7 @@ def algo_fp64_per_unit(eq: dict, basis: str = "contract") -> dict:
     return dict(particle=per_particle,
                 leaf=g + 1 + (1 if strat == 2 else 0),     # Π *= g (/ q)
                 split=split,
-                tree=3 + (1 if strat == 1 else 0))         # ΣC += C, ΣC² += C·C (× e^{λt})
+                tree=3 + (1 if strat == 1 else 0) + tree_g)   # ΣC += C, ΣC² += C·C (× e^{λt})
 
 
 def algo_fp64_ops(eq: dict, stats: dict, n_points: int = 1, basis: str = "contract") -> float:

@@ -271,8 +271,9 @@ static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, bool sb, bool sh
                            KernelFn* prod, int* smem, int* pool_cap) {
 #define RT_K(D, G)                                                              \
   if (dim == D && gk == G) {                                                    \
-    *smem = rtk::smem_bytes<D>();                                               \
-    *pool_cap = rtk::PoolCap<D>::v;                                             \
+    const bool ring = G == 2 && !f32 && !sh;   /* rtk::UseRing */                \
+    *smem = ring ? rtk::smem_bytes<D, true>() : rtk::smem_bytes<D, false>();    \
+    *pool_cap = ring ? rtk::PoolCap<D, true>::v : rtk::PoolCap<D, false>::v;    \
     if (sh && sb) {                                                             \
       *prod = pick_kernel<D, G, false, false, true, true>();                    \
       return rec ? pick_kernel<D, G, true, false, true, true>() : *prod;        \

@@ -28,8 +28,11 @@ def test_cost_model_per_unit_counts():
     assert u3["tree"] == 3 and u1["split"] == 1
     # Lorentzian g (cfg4): |x|² (2d-1) + /s² + 1 + reciprocal (div 8) + amp, then Π *= g
     assert u3["leaf"] == s3["leaf"] == 5 + 1 + 1 + 8 + 1 + 1
-    # Gaussian g (cfg2, d = 1): x² + /s² + exp 15 + amp, then Π *= g
-    assert u1["leaf"] == 1 + 1 + 15 + 1 + 1
+    # Gaussian g (cfg2, d = 1): the textbook per-leaf x² + /s² + exp 15 + amp,
+    # then Π *= g; the kernel's closed form — x², one FMA into
+    # the exponent sum, amp, Π *= amp per leaf; exp + 1 multiply per tree
+    assert s1["leaf"] == 1 + 1 + 15 + 1 + 1
+    assert u1["leaf"] == 1 + 1 + 1 + 1 and u1["tree"] == 3 + 15 + 1
     # FP32 positions: only the FP64 part (clock, weights, product, sums)
     u32 = bench.algo_fp64_per_unit(dict(W.get("cfg2")["eq"], precision=W.PREC_FP32_POS))
     assert u32["particle"] == (1 + 20) + (2 + 1) + 4 and u32["leaf"] == 1
@@ -66,8 +69,9 @@ def test_cost_model_strategies():
     ub = bench.algo_fp64_per_unit(W.get("ex1B")["eq"])        # Strategy B
     up = bench.algo_fp64_per_unit(dict(base, strategy=0), basis="survey")   # potential
     assert up["particle"] - ub["particle"] == 20 - 2
-    assert ua["split"] == up["split"] + 15 + 2 and ua["tree"] == up["tree"] + 1
-    assert ub["split"] == up["split"] + 1 and ub["leaf"] == up["leaf"] + 1
+    upc = bench.algo_fp64_per_unit(dict(base, strategy=0))   # potential, contract basis
+    assert ua["split"] == up["split"] + 15 + 2 and ua["tree"] == upc["tree"] + 1
+    assert ub["split"] == up["split"] + 1 and ub["leaf"] == upc["leaf"] + 1
 
 
 def test_clock_summary_from_nvidia_smi_rows():
