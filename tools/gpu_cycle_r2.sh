@@ -28,4 +28,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:tree
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tree_walk -s 1 -c 1 \
     -o gpurun_out/prof_tw_cfg2_$tag python bench.py --config cfg2 --steps 1 --warmup 1 --no-cpu-baseline --graph off \
     > gpurun_out/ncu_full_cfg2_$tag.log 2>&1
-echo done
+
+# keep the merge-back under gpurun's 64 MiB: compress the reports
+for f in gpurun_out/prof_tw_cfg4_$tag.ncu-rep gpurun_out/prof_tw_cfg2_$tag.ncu-rep; do
+  [ -f "$f" ] && xz -T0 -6 "$f"
+done
+du -sh gpurun_out
