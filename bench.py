@@ -52,7 +52,10 @@ N_SM, FP64_LANES, F_MAX_MHZ = 148, 64, 1965.0
 # transcendental or reciprocal, the amplitude) + 1 mul — Gaussian data on
 # independent FP64 trees: |x|², one FMA into the tree's exponent sum and the
 # amplitude per leaf, the exponential once per tree (the kernel's closed form,
-# DESIGN.md §4); per split: 1 mul; per tree: 1 mul + 2 adds.  The FP32-position variant is credited only its
+# DESIGN.md §4); per split: 1 mul (Strategy A's shift and variable
+# coefficients: their exponents and denominators accumulated per split, the
+# exponential and reciprocal once per tree — the same closed form); per
+# tree: 1 mul + 2 adds.  The FP32-position variant is credited only its
 # FP64 part (clock, weights, product, sums).  basis="survey" gives SURVEY
 # §8(d)'s original textbook count (reported beside it).
 SV = dict(log=20, exp=15, sqrt=8, div=8, tanh=25, sincospi=20)
@@ -84,20 +87,28 @@ def algo_fp64_per_unit(eq: dict, basis: str = "contract") -> dict:
          W.G_LORENTZ: r2 + 1 + 1 + SV["div"] + 1}[eq["init_kind"]]   # |x|², /s², 1 +, 1/·, amp
     if f32 and basis != "survey":
         g = 0                                              # g in single precision
+    var = any(eq.get("coef_kind", [0] * 9))
+    ring = not f32 and not eq.get("shared") and basis != "survey"
+    defer_g = ring and eq["init_kind"] == W.G_GAUSS
+    defer_w = ring and (strat == 1 or var)
+    # the kernel's closed forms (RingVals): exponential and
+    # rational factors are carried as an exponent sum X and a denominator
+    # product D and evaluated once per tree
     tree_g = 0
-    if eq["init_kind"] == W.G_GAUSS and not f32 and not eq.get("shared") and basis != "survey":
-        # the kernel's closed form (UseRing): a leaf adds
-        # |x|²/s² to the tree's exponent sum and multiplies amp in; the
-        # exponential is evaluated once per tree
-        g = r2 + 1 + 1                                     # |x|², fma into E, amp
-        tree_g = SV["exp"] + 1                             # exp(-E), × the tree product
+    if defer_g:
+        g = r2 + 1 + 1                                     # |x|², fma into X, amp
+    if defer_g or defer_w:
+        tree_g = SV["exp"] + 1                             # e^X, × the tree product
     split = 1                                              # Π *= w_k
     if strat == 1:
-        split += SV["exp"] + 2                             # e^{(k-1)λτ_c}
+        split += 2 if defer_w else SV["exp"] + 2           # e^{(k-1)λτ_c}: (k-1)λ, fma into X
+        tree_g += SV["div"] if defer_w else 0              # e^{+X} = 1 / e^{-X}
     if strat == 2:
         split += 1                                         # η(τ) = τ
-    if any(eq.get("coef_kind", [0] * 9)):
-        split += SV["exp"] + SV["div"] + 4                 # e^{-y²/s²}/(τ_c + t0)
+    if var:
+        # e^{-y²/s²}/(τ_c + t0): y², /s², X +=, τ_c + t0, D *= (deferred)
+        split += 5 if defer_w else SV["exp"] + SV["div"] + 4
+        tree_g += SV["div"] + 1 if defer_w else 0          # 1/D, ×
     return dict(particle=per_particle,
                 leaf=g + 1 + (1 if strat == 2 else 0),     # Π *= g (/ q)
                 split=split,

@@ -271,9 +271,11 @@ static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, bool sb, bool sh
                            KernelFn* prod, int* smem, int* pool_cap) {
 #define RT_K(D, G)                                                              \
   if (dim == D && gk == G) {                                                    \
-    const bool ring = G == 2 && !f32 && !sh;   /* rtk::UseRing */                \
-    *smem = ring ? rtk::smem_bytes<D, true>() : rtk::smem_bytes<D, false>();    \
-    *pool_cap = ring ? rtk::PoolCap<D, true>::v : rtk::PoolCap<D, false>::v;    \
+    const int rv = (f32 || sh) ? 0 : (gen ? 2 : (G == 2 ? 1 : 0));  /* rtk::RingVals */ \
+    *smem = rv == 2 ? rtk::smem_bytes<D, 2>() : rv == 1 ? rtk::smem_bytes<D, 1>()   \
+                    : rtk::smem_bytes<D, 0>();                                  \
+    *pool_cap = rv == 2 ? rtk::PoolCap<D, 2>::v : rv == 1 ? rtk::PoolCap<D, 1>::v   \
+                        : rtk::PoolCap<D, 0>::v;                                \
     if (sh && sb) {                                                             \
       *prod = pick_kernel<D, G, false, false, true, true>();                    \
       return rec ? pick_kernel<D, G, true, false, true, true>() : *prod;        \

@@ -105,10 +105,12 @@ template <int DIM> struct PoolBase;
 template <> struct PoolBase<1> { static constexpr int v = RT_POOL_D1; };
 template <> struct PoolBase<2> { static constexpr int v = RT_POOL_D2; };
 template <> struct PoolBase<3> { static constexpr int v = RT_POOL_D3; };
-template <int DIM, bool RING> struct PoolCap {
-  // the ring's kRing × 17 bytes come out of the pool's (DIM+2)·8 + 3 per entry
-  static constexpr int v = RING ? PoolBase<DIM>::v - (kRing * 17 + (DIM + 2) * 8 + 2) / ((DIM + 2) * 8 + 3)
-                                : PoolBase<DIM>::v;
+// RV = deferred values per ring record beside the tree product (RingVals):
+// the ring's kRing × (8 (1 + RV) + 1) bytes come out of the pool's
+// (DIM+2)·8 + 3 per entry
+template <int RV> __host__ __device__ constexpr int ring_bytes() { return RV > 0 ? kRing * (8 * (1 + RV) + 1) : 0; }
+template <int DIM, int RV> struct PoolCap {
+  static constexpr int v = PoolBase<DIM>::v - (ring_bytes<RV>() + (DIM + 2) * 8 + 2) / ((DIM + 2) * 8 + 3);
 };
 template <int DIM, bool REC> struct MinCtas {
   static constexpr int v = (DIM == 1 ? RT_CTAS_D1 : DIM == 2 ? RT_CTAS_D2 : RT_CTAS_D3) - (REC ? 1 : 0);
@@ -226,38 +228,43 @@ __device__ __forceinline__ float g_eval_f(const float (&x)[DIM], const WalkParam
   }
 }
 
-// Deferred Gaussian data (independent trees, FP64 positions; the "ring"
-// kernels): g = amp e^{-|x|²/s²} has Π_l g(x_l) = amp^L · exp(−Σ_l |x_l|²/s²),
-// so a leaf multiplies amp into the tree product and adds |x|²/s² to an
-// exponent sum E, and the exponential is evaluated once per TREE — when the
-// finished tree's record (order bin, product, E) is flushed from a per-warp
-// ring of kRing records, 32 at a time, one record per lane (every lane busy
-// on it, instead of an exponential per particle).  Measured: cfg2 +6.6 %,
-// cfg3 +3.5 %; the same ring with the Lorentzian's denominator product
-// Π(1 + |x|²/s²) and one reciprocal per tree made cfg4 0.9 % slower (its
-// reciprocal is cheap, the ring is not free), so other data evaluate g at
-// the leaf and send each finished tree straight to its REDs.
-template <int GK, bool F32, bool SH> __host__ __device__ constexpr bool UseRing() {
-  return GK == 2 && !F32 && !SH;
+// Deferred factors (independent trees, FP64 positions; the "ring" kernels).
+// Exponential and rational factors of a tree's product are carried in closed
+// form — an exponent sum X and a denominator product D, C = Π · e^X / D —
+// and evaluated once per TREE, when the finished tree's record (order bin,
+// Π, X[, D]) is flushed from a per-warp ring of kRing records, 32 at a time,
+// one record per lane (every lane busy on it, instead of the evaluation in
+// every particle iteration):
+//   Gaussian data g = amp e^{-|x|²/s²}: Π_l g(x_l) = amp^L e^{−Σ_l |x_l|²/s²}
+//     — a leaf multiplies amp into Π and adds −|x|²/s² to X;
+//   (general kernels, NEXT rows f2) Strategy A's shift factor e^{(k−1)λτ_c}
+//     per split adds (k−1)λτ_c to X; a variable coefficient
+//     b_k e^{−y_a²/s²}/(τ_c + t0) adds −y_a²/s² to X and multiplies τ_c + t0
+//     into D.
+// Measured: cfg2 +6.4 %, cfg3 +3.6 %; the same ring with the Lorentzian's
+// denominator product Π(1 + |x|²/s²) made cfg4 0.9 % slower (its reciprocal
+// is cheap, the ring is not free), so other data evaluate g at the leaf.
+// RingVals: 0 no ring, 1 Π and X (Gaussian, GEN = false), 2 Π, X and D (GEN).
+template <int GK, bool F32, bool SH, bool GEN> __host__ __device__ constexpr int RingVals() {
+  return (F32 || SH) ? 0 : (GEN ? 2 : (GK == 2 ? 1 : 0));
 }
 
 // per-warp shared memory: pool fields [DIM+2][cap] doubles, (ring: record
-// values [2][kRing] doubles), state, prev [cap] int16, free list [cap] u8,
-// (ring: record bins [kRing] u8)
-template <int DIM, bool RING>
+// values [1 + RV][kRing] doubles), state, prev [cap] int16, free list [cap]
+// u8, (ring: record bins [kRing] u8)
+template <int DIM, int RV>
 __host__ __device__ constexpr int warp_smem_bytes() {
-  return PoolCap<DIM, RING>::v * ((DIM + 2) * 8 + 2 + 1) + (RING ? kRing * (2 * 8 + 1) : 0) +
-         static_cast<int>(sizeof(WarpState));
+  return PoolCap<DIM, RV>::v * ((DIM + 2) * 8 + 2 + 1) + ring_bytes<RV>() + static_cast<int>(sizeof(WarpState));
 }
 
-template <int DIM, bool RING>
+template <int DIM, int RV>
 __host__ __device__ constexpr int warp_stride() {
-  return (warp_smem_bytes<DIM, RING>() + 15) / 16 * 16;
+  return (warp_smem_bytes<DIM, RV>() + 15) / 16 * 16;
 }
 
-template <int DIM, bool RING>
+template <int DIM, int RV>
 __host__ __device__ constexpr int smem_bytes() {
-  return 128 * 16 /* log table */ + kWarpsPerCta * warp_stride<DIM, RING>() +
+  return 128 * 16 /* log table */ + kWarpsPerCta * warp_stride<DIM, RV>() +
          9 * 8 + 9 * 4 + 4 /* offspring weights and sizes */ + 32 * 8 /* exp table */;
 }
 
@@ -307,8 +314,9 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   using PT = typename std::conditional<F32, float, double>::type;   // position type
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int NF = DIM + 2;
-  constexpr bool RING = UseRing<GK, F32, SH>();
-  constexpr int CAP = PoolCap<DIM, RING>::v;
+  constexpr int RV = RingVals<GK, F32, SH, GEN>();
+  constexpr bool RING = RV > 0;
+  constexpr int CAP = PoolCap<DIM, RV>::v;
   // lane, its lower-lanes mask and the warp's shared-memory offset are read
   // through opaque moves, so the compiler keeps them in registers instead of
   // rematerialising them from threadIdx every iteration
@@ -320,14 +328,15 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 
   // ---- shared memory carve-up -------------------------------------------
   LogEntry* const ltab = reinterpret_cast<LogEntry*>(smem_raw);
-  const int wstride = warp_stride<DIM, RING>();
+  const int wstride = warp_stride<DIM, RV>();
   unsigned woff;
   asm volatile("mov.u32 %0, %1;" : "=r"(woff) : "r"(128 * 16 + wib * wstride));
   unsigned char* const wbase = smem_raw + woff;
   double* const pool = reinterpret_cast<double*>(wbase);                   // [NF][CAP]
   double* const rval = pool + NF * CAP;                                    // ring: [kRing] tree products
-  double* const rexp = rval + kRing;                                       // ring: [kRing] exponent sums
-  WarpState* const ws = reinterpret_cast<WarpState*>(RING ? rexp + kRing : rval);
+  double* const rexp = rval + kRing;                                       // ring: [kRing] exponent sums X
+  double* const rden = rexp + kRing;                                       // ring (RV = 2): [kRing] denominators D
+  WarpState* const ws = reinterpret_cast<WarpState*>(rval + (RING ? kRing * (1 + RV) : 0));
   int16_t* const prevS = reinterpret_cast<int16_t*>(ws + 1);               // [CAP]
   uint8_t* const freeS = reinterpret_cast<uint8_t*>(prevS + CAP);           // [CAP]
   uint8_t* const rbin = freeS + CAP;                                       // ring: [kRing] order bins
@@ -336,7 +345,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   int* const ktab = reinterpret_cast<int*>(wtab + 9);                     // [9] offspring k
   double* const etab = wtab + 14;                                         // [32] 2^(j/32)
   for (int q = threadIdx.x; q < 128; q += kThreads) ltab[q] = kLogTable[q];
-  if constexpr (GK == 2 && !F32) {
+  if constexpr ((GK == 2 && !F32) || RING) {
     if (threadIdx.x < 32) etab[threadIdx.x] = kExpT32[threadIdx.x];
   }
   if (threadIdx.x < 9) {
@@ -411,7 +420,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
 #pragma unroll
   for (int k = 0; k < DIM; ++k) y[k] = PT(0);
   double tau = 0.0, Pi = 1.0;
-  double gexp = 0.0;                   // ring: Σ |x_l|²/s² over the tree's leaves (UseRing)
+  double gexp = 0.0, gden = 1.0;       // ring: the tree's deferred exponent X and denominator D (RingVals)
   uint64_t label = 1;
   int ne = 0, top = -1;                // top: the lane's top stack entry (-1: empty)
   int leaves = 0, parts = 0;           // per-tree counts (trace variant only)
@@ -426,6 +435,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     for (int k = 0; k < DIM; ++k) y[k] = SH ? PT(0) : static_cast<PT>(ws->iss_y[k]);   // SH: δ = 0
     tau = P.t; label = 1; Pi = GEN ? P.root : 1.0; ne = 0; top = -1;   // (GEN = false: no shift, root factor 1)
     if constexpr (RING) gexp = 0.0;
+    if constexpr (RV == 2) gden = 1.0;
     if constexpr (REC || SH) { leaves = 0; parts = 0; }
     if constexpr (SH && sh_moments<GK>()) {
 #pragma unroll
@@ -435,10 +445,22 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     active = true;
   };
 
-  // The tree's contribution C from its record: product × deferred leaf factor
-  auto tree_c = [&](double pi, double ex) -> double {
-    if constexpr (RING) return pi * exp_neg_tab(-ex, etab);
-    else return pi;
+  // The tree's contribution C = Π e^X / D from its record (RingVals)
+  auto tree_c = [&](double pi, double x, double dn) -> double {
+    if constexpr (RING) {
+      double e;
+      if constexpr (RV == 1) {
+        e = exp_neg_tab(x, etab);                // (Gaussian data: X <= 0)
+      } else {
+        const double en = exp_neg_tab(-fabs(x), etab);
+        e = x > 0.0 ? rcp_nr(en) : en;
+        e *= rcp_nr(dn);
+      }
+      const double c = pi * e;
+      return pi == 0.0 ? 0.0 : c;                // (a killed tree: no 0 · inf)
+    } else {
+      return pi;
+    }
   };
   // Record ring: rn records from slot rhead on (warp-uniform counters).
   // flush(m): lane i < m adds record rhead + i — C, C² and 1 — to ITS OWN
@@ -452,7 +474,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       const int sl = (rhead + lane) & (kRing - 1);
       const int b = rbin[sl];
       RT_CHECK(b >= 0 && b < P.nb);
-      const double c = tree_c(rval[sl], rexp[sl]);
+      const double c = tree_c(rval[sl], rexp[sl], RV == 2 ? rden[sl] : 1.0);
       double* a = lacc() + b * 96;
       red_add_keep(a, c, pol);
       red_add_keep(a + 32, c * c, pol);
@@ -668,12 +690,12 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     double gv;                                  // g at the leaf
     if constexpr (F32) {
       gv = static_cast<double>(g_eval_f<DIM, GK>(y, P));
-    } else if constexpr (RING) {               // Gaussian: exponent deferred to the record (UseRing)
+    } else if constexpr (RING && GK == 2) {    // Gaussian: exponent deferred to the record (RingVals)
       double r2 = y[0] * y[0];
       if constexpr (DIM >= 2) r2 = fma(y[1], y[1], r2);
       if constexpr (DIM >= 3) r2 = fma(y[2], y[2], r2);
       gv = P.amp;
-      const double e = fma(r2, P.inv_scale2, gexp);
+      const double e = fma(-r2, P.inv_scale2, gexp);
       gexp = leaf ? e : gexp;
     } else if constexpr (GK == 2) {             // Gaussian (shared trees: unused)
       double r2 = y[0] * y[0];
@@ -686,7 +708,20 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
     const int k = ktab[s];
     double wk = wtab[s];
     if constexpr (SB) wk *= tau;                // η(τ) = τ
-    if (GEN && P.wmode != 0) {                  // warp-uniform: f2/f3 weight factors
+    if (RV == 2 && P.wmode != 0) {              // warp-uniform: f2/f3 weight factors, deferred
+      // into the tree's X and D (RingVals): the same factors, evaluated once per tree
+      double x = 0.0, dn = 1.0;
+      if ((P.var_s >> s) & 1u) {                // c_k(y, τ_c) = b_k e^{-y_a²/s²}/(τ_c + t0)
+        double ya = static_cast<double>(y[0]);   // (no dynamic register indexing)
+        if constexpr (DIM >= 2) if (P.coef_axis == 1) ya = static_cast<double>(y[1]);
+        if constexpr (DIM >= 3) if (P.coef_axis == 2) ya = static_cast<double>(y[2]);
+        x = -(ya * ya) * P.coef_inv_s2;
+        dn = tc + P.coef_t0;
+      }
+      if (P.wmode & 2) x = fma(static_cast<double>(k - 1) * P.lam, tc, x);   // e^{(k-1)λτ_c}
+      gexp = leaf ? gexp : gexp + x;
+      gden = leaf ? gden : gden * dn;
+    } else if (GEN && P.wmode != 0) {           // warp-uniform: f2/f3 weight factors
       double f = 1.0;
       if ((P.var_s >> s) & 1u) {                // c_k(y, τ_c) = b_k e^{-y_a²/s²}/(τ_c + t0)
         double ya = static_cast<double>(y[0]);   // (no dynamic register indexing)
@@ -849,7 +884,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
       if (done && (rel & ((1u << P.rec_shift) - 1u)) == 0u) {
         TreeRec r;
         r.ne = ne; r.leaves = leaves; r.particles = parts; r.pruned = pruned ? 1 : 0;
-        r.C = pruned ? 0.0 : tree_c(Pi, gexp);
+        r.C = pruned ? 0.0 : tree_c(Pi, gexp, gden);
         P.recs[static_cast<int64_t>(iss_node) * P.n_rec + (rel >> P.rec_shift)] = r;
       }
     }
@@ -915,6 +950,7 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
             rbin[sl] = static_cast<uint8_t>(ne);
             rval[sl] = Pi;
             rexp[sl] = gexp;
+            if constexpr (RV == 2) rden[sl] = gden;
           }
           rn += nfin;
           if (rn >= 32) flush(32);

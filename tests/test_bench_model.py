@@ -70,7 +70,14 @@ def test_cost_model_strategies():
     up = bench.algo_fp64_per_unit(dict(base, strategy=0), basis="survey")   # potential
     assert up["particle"] - ub["particle"] == 20 - 2
     upc = bench.algo_fp64_per_unit(dict(base, strategy=0))   # potential, contract basis
-    assert ua["split"] == up["split"] + 15 + 2 and ua["tree"] == upc["tree"] + 1
+    us = bench.algo_fp64_per_unit(base, basis="survey")      # shift, textbook: e^{(k-1)λτ_c} per split
+    assert us["split"] == up["split"] + 15 + 2
+    # the kernel's closed form: (k-1)λ and an FMA into the
+    # exponent sum per split; the root factor, and e^{+X} = 1/e^{-X} per tree
+    assert ua["split"] == upc["split"] + 2 and ua["tree"] == upc["tree"] + 1 + 8
+    # variable coefficients: y², /s², X +=, τ_c + t0, D *= per split; 1/D and × per tree
+    uv = bench.algo_fp64_per_unit(W.get("ex5A")["eq"])
+    assert uv["split"] == 1 + 2 + 5 and uv["tree"] == 3 + 1 + (15 + 1) + 8 + (8 + 1)
     assert ub["split"] == up["split"] + 1 and ub["leaf"] == upc["leaf"] + 1
 
 

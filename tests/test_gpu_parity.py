@@ -403,8 +403,13 @@ def test_host_api_equals_device_api(P):
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg4", "heat_d2_tanh", "B_cfg2_k1", "ex2_B"])
 def test_specialised_kernel_equals_general(P, monkeypatch, name):
     """The GEN = false tree walk (no f2/f3 weight factors, 1-3 offspring kinds)
-    performs the general kernel's arithmetic: sums and per-tree records are
-    bitwise equal (RT_FORCE_GEN=1 selects the general kernel)."""
+    performs the general kernel's arithmetic: per-tree records are bitwise
+    equal (RT_FORCE_GEN=1 selects the general kernel).  So are the sums where
+    both kernels send finished trees through the record ring (Gaussian data,
+    DESIGN.md §4); otherwise the general kernel's ring assigns trees to other
+    lanes' accumulators than the specialised kernel's direct REDs, which
+    changes only the summation order (counts exact, sums of same-sign C to
+    1e-13)."""
     eq, pts, t, N = CASES[name]
     x = dev(pts)
     a = P.Estimator(eq).sums(x, t, 4 * N, seed=3).cpu().numpy()
@@ -412,8 +417,13 @@ def test_specialised_kernel_equals_general(P, monkeypatch, name):
     monkeypatch.setenv("RT_FORCE_GEN", "1")
     b = P.Estimator(eq).sums(x, t, 4 * N, seed=3).cpu().numpy()
     rb, _ = P.Estimator(eq).trace(x, t, N, seed=4)
-    assert np.array_equal(a, b)
     assert np.array_equal(ra, rb)
+    if eq["init_kind"] == W.G_GAUSS:
+        assert np.array_equal(a, b)
+    else:
+        assert np.array_equal(a[:, :, 2], b[:, :, 2])
+        assert eq["init_amp"] > 0
+        assert np.all(np.abs(a[:, :, :2] - b[:, :, :2]) <= 1e-13 * np.abs(b[:, :, :2]))
 
 
 def test_host_call_after_async_dev_call(P):
