@@ -265,47 +265,33 @@ static KernelFn pick_kernel() {
   return rtk::tree_walk_kernel<DIM, GK, REC, F32, SB, SH, GEN>;
 }
 
-// The kernel for (dim, g, rec) and the production (rec = false) kernel whose
+// The production (rec = false) kernel of one instantiation and, for rec,
+// its record-emitting twin (launched on the production kernel's geometry),
+// with the shared memory and stack-pool size of that instantiation's layout
+// (rtk::RingVals decides whether it carries the finished-tree record ring).
+template <int D, int G, bool F32, bool SB, bool SH, bool GEN>
+static KernelFn pick(bool rec, KernelFn* prod, int* smem, int* pool_cap) {
+  constexpr int rv = rtk::RingVals<G, F32, SH, GEN>();
+  *smem = rtk::smem_bytes<D, rv>();
+  *pool_cap = rtk::PoolCap<D, rv>::v;
+  *prod = pick_kernel<D, G, false, F32, SB, SH, GEN>();
+  return rec ? pick_kernel<D, G, true, F32, SB, SH, GEN>() : *prod;
+}
+
+// The kernel for (dim, g, rec, variant) and the production kernel whose
 // occupancy fixes the launch geometry for both.
 static KernelFn kernel_for(int dim, int gk, bool rec, bool f32, bool sb, bool sh, bool gen,
                            KernelFn* prod, int* smem, int* pool_cap) {
-#define RT_K(D, G)                                                              \
-  if (dim == D && gk == G) {                                                    \
-    const int rv = (f32 || sh) ? 0 : (gen ? 2 : (G == 2 ? 1 : 0));  /* rtk::RingVals */ \
-    *smem = rv == 2 ? rtk::smem_bytes<D, 2>() : rv == 1 ? rtk::smem_bytes<D, 1>()   \
-                    : rtk::smem_bytes<D, 0>();                                  \
-    *pool_cap = rv == 2 ? rtk::PoolCap<D, 2>::v : rv == 1 ? rtk::PoolCap<D, 1>::v   \
-                        : rtk::PoolCap<D, 0>::v;                                \
-    if (sh && sb) {                                                             \
-      *prod = pick_kernel<D, G, false, false, true, true>();                    \
-      return rec ? pick_kernel<D, G, true, false, true, true>() : *prod;        \
-    }                                                                           \
-    if (sh) {                                                                   \
-      *prod = pick_kernel<D, G, false, false, false, true>();                   \
-      return rec ? pick_kernel<D, G, true, false, false, true>() : *prod;       \
-    }                                                                           \
-    if (sb && !gen) {                                                           \
-      *prod = pick_kernel<D, G, false, false, true, false, false>();            \
-      return rec ? pick_kernel<D, G, true, false, true, false, false>() : *prod; \
-    }                                                                           \
-    if (sb) {                                                                   \
-      *prod = pick_kernel<D, G, false, false, true>();                          \
-      return rec ? pick_kernel<D, G, true, false, true>() : *prod;              \
-    }                                                                           \
-    if (f32 && !gen) {                                                          \
-      *prod = pick_kernel<D, G, false, true, false, false, false>();            \
-      return rec ? pick_kernel<D, G, true, true, false, false, false>() : *prod; \
-    }                                                                           \
-    if (f32) {                                                                  \
-      *prod = pick_kernel<D, G, false, true, false>();                          \
-      return rec ? pick_kernel<D, G, true, true, false>() : *prod;              \
-    }                                                                           \
-    if (!gen) {                                                                 \
-      *prod = pick_kernel<D, G, false, false, false, false, false>();           \
-      return rec ? pick_kernel<D, G, true, false, false, false, false>() : *prod; \
-    }                                                                           \
-    *prod = pick_kernel<D, G, false, false, false>();                           \
-    return rec ? pick_kernel<D, G, true, false, false>() : *prod;               \
+#define RT_K(D, G)                                                                      \
+  if (dim == D && gk == G) {                                                            \
+    if (sh && sb) return pick<D, G, false, true, true, true>(rec, prod, smem, pool_cap);   \
+    if (sh) return pick<D, G, false, false, true, true>(rec, prod, smem, pool_cap);        \
+    if (sb && !gen) return pick<D, G, false, true, false, false>(rec, prod, smem, pool_cap); \
+    if (sb) return pick<D, G, false, true, false, true>(rec, prod, smem, pool_cap);        \
+    if (f32 && !gen) return pick<D, G, true, false, false, false>(rec, prod, smem, pool_cap); \
+    if (f32) return pick<D, G, true, false, false, true>(rec, prod, smem, pool_cap);       \
+    if (!gen) return pick<D, G, false, false, false, false>(rec, prod, smem, pool_cap);    \
+    return pick<D, G, false, false, false, true>(rec, prod, smem, pool_cap);               \
   }
   RT_K(1, 0) RT_K(1, 1) RT_K(1, 2) RT_K(1, 3)
   RT_K(2, 0) RT_K(2, 1) RT_K(2, 2) RT_K(2, 3)
