@@ -28,7 +28,7 @@ def test_parity_suite_under_bounds_checks():
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
                         os.path.join(HERE, "test_gpu_parity.py"), os.path.join(HERE, "test_gpu_pdd.py"),
                         os.path.join(HERE, "test_gpu_fuzz.py"),
-                        "-k", "tree_parity or pool or extreme or geometry or pdd_downstream or edge or chunks"],
+                        "-k", "tree_parity or pool or extreme or geometry or pdd_downstream or edge or chunks or ring"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     tail = r.stdout.strip().splitlines()[-1]

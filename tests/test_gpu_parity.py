@@ -305,6 +305,28 @@ def test_geometry_and_determinism(P):
     assert_nodes_close(d[:, :, 0], a[:, :, 0], rtol=1e-12, what="one CTA")
 
 
+@pytest.mark.parametrize("name", ["cfg2", "shift_ex5_d2"])
+def test_record_ring_task_boundaries(P, orc, name):
+    """The finished-tree record ring (RingVals: Gaussian data,
+    deferred split factors) flushes 32 records at a time and the rest at each
+    task close: task sizes below, at and around one and two flushes (1, 31,
+    32, 33, 64, 65 trees), one CTA (the ring then wraps many times) — counts
+    exact and sums at the node bar against the oracle."""
+    eq, pts, t, N = CASES[name]
+    pts = pts[:4]
+    x = dev(pts)
+    s_ref, _ = orc.sums(eq, pts, t, 700, seed=55)
+    absC = abs_sums(orc.trees(eq, pts, t, 700, seed=55), eq["K"])
+    est = P.Estimator(eq)
+    for tpt in (1, 31, 32, 33, 64, 65):
+        for grid in (0, 1):
+            est.set_launch(grid_ctas=grid, trees_per_task=tpt)
+            g = est.sums(x, t, 700, seed=55).cpu().numpy()
+            assert np.array_equal(g[:, :, 2], s_ref[:, :, 2]), (tpt, grid)
+            assert_sum_c_close(g[:, :, 0], s_ref[:, :, 0], absC, what=f"T={tpt} grid={grid}")
+            assert_nodes_close(g[:, :, 1], s_ref[:, :, 1], what=f"sum C^2 T={tpt}")
+
+
 @pytest.mark.parametrize("name,pool", [("cfg4", 1), ("cfg4", 9), ("cfg2_t2", 3), ("d3_gauss", 40),
                                        ("B_d3_var", 2), ("sh_cfg4", 5)])
 def test_stack_pool_overflow(P, orc, name, pool):
