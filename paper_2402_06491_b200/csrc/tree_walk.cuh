@@ -83,13 +83,13 @@ template <int GK> __host__ __device__ constexpr bool sh_moments() { return GK ==
 // give its 1 KB per warp up from the pool.
 // (RT_POOL_D<d> / RT_CTAS_D<d>: compile-time overrides for occupancy sweeps)
 #ifndef RT_POOL_D1
-#define RT_POOL_D1 192
+#define RT_POOL_D1 182
 #endif
 #ifndef RT_POOL_D2
-#define RT_POOL_D2 176
+#define RT_POOL_D2 168
 #endif
 #ifndef RT_POOL_D3
-#define RT_POOL_D3 144
+#define RT_POOL_D3 138
 #endif
 #ifndef RT_CTAS_D1
 #define RT_CTAS_D1 8
@@ -182,7 +182,7 @@ struct WarpState {
   int gtop, gfree;          // overflow area: bump pointer, free-list size
   double* gpool;            // the warp's overflow area (read in the slow paths only,
   int* gprev;               //   so the compiler does not keep or rematerialise them)
-  double* lacc;             // the warp's lane accumulators
+  double* lacc[32];         // each lane's accumulator base (its [bin 0][ΣC] word)
 };
 
 // The initial data g: constant, tanh step, Gaussian,
@@ -360,11 +360,13 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   if (lane == 0) {
     ws->gpool = P.gpool + static_cast<int64_t>(gwarp) * P.gcap * NF;
     ws->gprev = P.gaux + static_cast<int64_t>(gwarp) * 2 * P.gcap;
-    ws->lacc = SH ? nullptr : P.lacc + static_cast<int64_t>(gwarp) * P.nb * 96;
   }
+  ws->lacc[lane] = SH ? nullptr : P.lacc + static_cast<int64_t>(gwarp) * P.nb * 96 + lane;
   __syncwarp();
   // lane-private order-bin accumulators in global memory: [bin][ΣC, ΣC², n][lane]
-  auto lacc = [&]() -> double* { return *static_cast<double* volatile*>(&ws->lacc) + lane; };
+  // (the lane's base read back from shared memory where used: one 64-bit
+  // load and one wide multiply-add per address, no register held)
+  auto lacc = [&]() -> double* { return *static_cast<double* volatile*>(&ws->lacc[lane]); };
   if constexpr (!SH) {
     double* a = lacc();
     for (int b = 0; b < P.nb; ++b) { a[b * 96] = 0.0; a[b * 96 + 32] = 0.0; a[b * 96 + 64] = 0.0; }
