@@ -310,4 +310,31 @@ RTM_HD double exp_neg_tab(double x, const double* T) {
   return x < -745.5 ? 0.0 : (p * s1) * s2;
 }
 
+// a · e^x for finite a and any x (the record-ring trees' C = Π e^X, DESIGN.md
+// §4): the table-driven e^x = 2^m T_j (1 + (e^r − 1)) of exp_neg_tab with the
+// power 2^m applied to the PRODUCT last, in two exact halves — neither e^x
+// nor a needs to be representable on its own, only the result (x clamped to
+// ±1400, where 2^m's halves are still normal).  Same rounding as a ·
+// exp_neg_tab(x) wherever e^x is normal.
+RTM_HD double mul_exp_tab(double a, double x, const double* T) {
+  const double xc = x < -1400.0 ? -1400.0 : (x > 1400.0 ? 1400.0 : x);
+  const double kf = rint_d(xc * kExp32Inv);
+  double r = fma_d(kf, -kExp32Hi, xc);
+  r = fma_d(kf, -kExp32Lo, r);
+  double q = kExpQ[5];
+  q = fma_d(q, r, kExpQ[4]);
+  q = fma_d(q, r, kExpQ[3]);
+  q = fma_d(q, r, kExpQ[2]);
+  q = fma_d(q, r, kExpQ[1]);
+  q = fma_d(q, r, kExpQ[0]);
+  const int k = static_cast<int>(kf);
+  const double t = T[k & 31];
+  const double p = fma_d(t, q * r, t);
+  const int m = (k - (k & 31)) / 32;   // floor(k / 32), exact; |m| <= 2020
+  const int m1 = m / 2, m2 = m - m1;   // |m1|, |m2| <= 1010: 2^m1, 2^m2 normal
+  const double s1 = dfrom(static_cast<uint64_t>(1023 + m1) << 52);
+  const double s2 = dfrom(static_cast<uint64_t>(1023 + m2) << 52);
+  return ((a * p) * s1) * s2;
+}
+
 }  // namespace rtk

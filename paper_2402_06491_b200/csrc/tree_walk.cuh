@@ -448,18 +448,11 @@ tree_walk_kernel(const __grid_constant__ WalkParams P) {
   };
 
   // The tree's contribution C = Π e^X / D from its record (RingVals)
+  // (Π e^X with the power of two applied last: no overflow of e^X alone)
   auto tree_c = [&](double pi, double x, double dn) -> double {
     if constexpr (RING) {
-      double e;
-      if constexpr (RV == 1) {
-        e = exp_neg_tab(x, etab);                // (Gaussian data: X <= 0)
-      } else {
-        const double en = exp_neg_tab(-fabs(x), etab);
-        e = x > 0.0 ? rcp_nr(en) : en;
-        e *= rcp_nr(dn);
-      }
-      const double c = pi * e;
-      return pi == 0.0 ? 0.0 : c;                // (a killed tree: no 0 · inf)
+      const double a = RV == 2 ? pi * rcp_nr(dn) : pi;
+      return mul_exp_tab(a, x, etab);
     } else {
       return pi;
     }

@@ -19,6 +19,7 @@ __global__ void math_kernel(int which, const double* x, long n, double* y, doubl
     case 6: sincos2pi_u32(static_cast<uint32_t>(x[q]), y[q], z[q]); break;
     case 7: y[q] = cos2pi_u32(static_cast<uint32_t>(x[q])); break;
     case 8: y[q] = exp_neg_tab(x[q], kExpT32); break;
+    case 9: y[q] = mul_exp_tab(z[q], x[q], kExpT32); break;   // z: the factor a
     default: y[q] = exp_neg(x[q]); break;
   }
 }
@@ -27,6 +28,7 @@ extern "C" int math_dev(int which, const double* hx, long n, double* hy, double*
   double *x, *y, *z;
   if (cudaMalloc(&x, n * 8) || cudaMalloc(&y, n * 8) || cudaMalloc(&z, n * 8)) return 1;
   cudaMemcpy(x, hx, n * 8, cudaMemcpyHostToDevice);
+  if (hz) cudaMemcpy(z, hz, n * 8, cudaMemcpyHostToDevice);   // (case 9: the factor a)
   math_kernel<<<(n + 255) / 256, 256>>>(which, x, n, y, z);
   cudaError_t e = cudaMemcpy(hy, y, n * 8, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess && hz) e = cudaMemcpy(hz, z, n * 8, cudaMemcpyDeviceToHost);

@@ -13,4 +13,5 @@ void m_sqrt_pos(const double* x, long n, double* y) { for (long i = 0; i < n; ++
 void m_rcp(const double* x, long n, double* y) { for (long i = 0; i < n; ++i) y[i] = rcp_nr(x[i]); }
 void m_exp(const double* x, long n, double* y) { for (long i = 0; i < n; ++i) y[i] = exp_neg(x[i]); }
 void m_exp_tab(const double* x, long n, double* y) { for (long i = 0; i < n; ++i) y[i] = exp_neg_tab(x[i], kExpT32); }
+void m_mul_exp(const double* a, const double* x, long n, double* y) { for (long i = 0; i < n; ++i) y[i] = mul_exp_tab(a[i], x[i], kExpT32); }
 }

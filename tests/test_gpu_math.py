@@ -27,10 +27,10 @@ def dev():
     return lib
 
 
-def _run(lib, which, x):
+def _run(lib, which, x, a=None):
     x = np.ascontiguousarray(x, dtype=np.float64)
     y = np.empty_like(x)
-    z = np.empty_like(x)
+    z = np.empty_like(x) if a is None else np.ascontiguousarray(a, dtype=np.float64).copy()
     assert lib.math_dev(which, x.ctypes.data, x.size, y.ctypes.data, z.ctypes.data) == 0
     return y, z
 
@@ -70,6 +70,25 @@ def test_device_sqrt_rcp_exp(dev):
     assert float(np.max(np.abs(v - ref) / ref)) < 4 * EPS
     w, _ = _run(dev, 8, e)                              # the table-driven exp (shared trees)
     assert float(np.max(np.abs(w - ref) / ref)) < 4 * EPS
+
+
+def test_device_mul_exp(dev):
+    """a · e^x as the record-ring flush evaluates a tree's C = Π e^X (DESIGN.md
+    §4): relative error < 4 eps over |x| <= 1400 whenever the product is a
+    normal number, though e^x alone over- or underflows (the round-1 form
+    1/e^{-x} turned x > 745 into NaN)."""
+    rng = np.random.default_rng(8)
+    x = rng.uniform(-1400, 1400, 400_000)
+    loga = rng.uniform(-700, 700, x.size)
+    keep = np.abs(x + loga) < 700                         # the product is a normal number
+    x, loga = x[keep], loga[keep]
+    a = np.exp(loga) * rng.choice([-1.0, 1.0], x.size)
+    y, _ = _run(dev, 9, x, a)
+    ref = a.astype(np.longdouble) * np.exp(x.astype(np.longdouble))
+    assert np.all(np.isfinite(y))
+    assert float(np.max(np.abs(y - ref) / np.abs(ref))) < 4 * EPS
+    z, _ = _run(dev, 9, np.array([-5.0, 0.0, 3.0]), np.zeros(3))
+    assert np.all(z == 0.0)
 
 
 def test_device_u32_angles_bitwise(dev):

@@ -160,6 +160,30 @@ def test_exp_neg(m):
     assert _call(m, "m_exp", np.array([-800.0]))[0] == 0.0
 
 
+def test_mul_exp_tab(m):
+    """a · e^x with the power of two applied to the product (the record-ring
+    trees' C = Π e^X): < 4 eps wherever the product is normal, over |x| <=
+    1400 (e^x alone over- or underflows beyond ±709); equal to a ·
+    exp_neg_tab(x) bit for bit where e^x is normal and a is a power of two."""
+    rng = np.random.default_rng(9)
+    x = rng.uniform(-1400, 1400, 400_000)
+    loga = rng.uniform(-700, 700, x.size)
+    keep = np.abs(x + loga) < 700
+    x, loga = x[keep], loga[keep]
+    a = np.exp(loga) * rng.choice([-1.0, 1.0], x.size)
+    m.m_mul_exp.argtypes = [C.c_void_p, C.c_void_p, C.c_long, C.c_void_p]
+    y = np.empty_like(x)
+    m.m_mul_exp(a.ctypes.data, x.ctypes.data, x.size, y.ctypes.data)
+    ref = a.astype(np.longdouble) * np.exp(x.astype(np.longdouble))
+    assert np.all(np.isfinite(y))
+    assert float(np.max(np.abs(y - ref) / np.abs(ref))) < 4 * EPS
+    xs = -rng.uniform(0, 700, 10_000)
+    ones = np.ldexp(1.0, rng.integers(-60, 60, xs.size)).astype(np.float64)
+    y1 = np.empty_like(xs)
+    m.m_mul_exp(ones.ctypes.data, xs.ctypes.data, xs.size, y1.ctypes.data)
+    assert np.array_equal(y1, ones * _call(m, "m_exp_tab", xs))
+
+
 def test_exp_neg_tab(m):
     """The table-driven exp (shared-tree phase 2): same bound and domain as
     exp_neg, including every table entry's neighbourhood, the subnormal range
