@@ -323,7 +323,8 @@ static rt_status plan_launch(rt_handle* h, KernelFn fn, int smem, int64_t n_poin
     // (not of the grid) so results are bitwise identical on any GPU size.
     // ~16 tasks per warp of a 4096-warp grid bound the end-of-launch tail;
     // >= 1024 trees keep the per-task drain (idle lanes while a task's last
-    // trees finish) to a few percent; <= 16384 keeps tails short.  Small
+    // trees finish) to a few percent; <= 32768 keeps the launch's end tail
+    // short (cfg4, task sizes 2048 … 65536 measured: 32768 best).  Small
     // workloads (< 4096 x 1024 trees) are latency-bound: there the floor
     // drops so that every warp of a 4096-warp grid gets about one task (a
     // multiple of 32 trees, at least 128).
@@ -331,7 +332,7 @@ static rt_status plan_launch(rt_handle* h, KernelFn fn, int smem, int64_t n_poin
         1024, std::max<int64_t>(128, (total / 4096 + 31) / 32 * 32));
     T = total / (int64_t(4096) * 16);
     T = std::max<int64_t>(T, floor_T);
-    T = std::min<int64_t>(T, 16384);
+    T = std::min<int64_t>(T, 32768);
   }
   T = std::min<int64_t>(T, n_trees);
   // task ids are 32-bit in the kernel: grow tasks until they number < 2^31
