@@ -305,8 +305,41 @@ struct Launch {
   int64_t T, tpn, n_tasks;
 };
 
+// Expected particles per tree of the equation at horizon t — used ONLY to
+// size tasks (a function of the workload, never of the GPU).  Exponential
+// clock at rate λ, offspring k with probability p̂_k, mean m̄ = Σ k p̂_k: the
+// branching process has E[leaves](t) = e^{λ(m̄−1)t} and E[splits] =
+// (E[leaves] − 1)/(m̄ − 1) (λt at m̄ = 1); Strategy B (leaf with probability
+// q) has E[particles] = 1/(1 − (1−q) m̄).  Pruning at K caps it near
+// 1 + K·k_max.
+static double expected_particles(const rt_handle* h, double t) {
+  const Norm& nz = h->nz;
+  const rt_eq_params& p = h->p;
+  if (nz.n_support == 0) return 1.5;
+  double m = 0.0;
+  int kmax = 0;
+  uint64_t prev = 0;
+  for (int s = 0; s < nz.n_support; ++s) {
+    m += nz.support[s] * (static_cast<double>(nz.thresh[s] - prev) / 4294967296.0);
+    prev = nz.thresh[s];
+    kmax = std::max(kmax, nz.support[s]);
+  }
+  const double cap = 1.0 + static_cast<double>(p.K) * std::max(1, kmax);
+  double e;
+  if (p.strategy == RT_STRATEGY_B) {
+    const double r = (1.0 - nz.q_hat) * m;
+    e = r < 1.0 ? 1.0 / (1.0 - r) : cap;
+  } else if (std::fabs(m - 1.0) < 1e-9) {
+    e = 1.0 + nz.lambda * t;
+  } else {
+    const double leaves = std::exp(std::min(50.0, nz.lambda * (m - 1.0) * t));
+    e = leaves + (leaves - 1.0) / (m - 1.0);
+  }
+  return std::max(1.0, std::min(e, cap));
+}
+
 static rt_status plan_launch(rt_handle* h, KernelFn fn, int smem, int64_t n_points,
-                             int64_t n_trees, Launch& L) {
+                             int64_t n_trees, double t, Launch& L) {
   int dev = 0, nsm = 0, per_sm = 0;
   RT_CUDA(cudaGetDevice(&dev));
   RT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -321,9 +354,13 @@ static rt_status plan_launch(rt_handle* h, KernelFn fn, int smem, int64_t n_poin
     // Warps fetch tasks dynamically and run each from a clean start, so a
     // task's sums depend on T alone; T is a function of the workload only
     // (not of the grid) so results are bitwise identical on any GPU size.
-    // ~16 tasks per warp of a 4096-warp grid bound the end-of-launch tail;
-    // >= 1024 trees keep the per-task drain (idle lanes while a task's last
-    // trees finish) to a few percent; <= 32768 keeps the launch's end tail
+    // A task costs a fixed close (read-back, butterfly, partials) and a
+    // clean-start tail; the launch ends with about half a task of
+    // imbalance.  Balancing the two gives T ~ sqrt(c · trees / particles
+    // per tree) (c = 0.6 fitted to task-size sweeps of cfg2, cfg3 and cfg5
+    // at t = 0.25 and 2, profiles/r2/tsweep.md), and no fewer than ~16
+    // tasks per warp of a 4096-warp grid's trees; >= 1024 trees keep the
+    // per-task drain to a few percent; <= 32768 keeps the launch's end tail
     // short (cfg4, task sizes 2048 … 65536 measured: 32768 best).  Small
     // workloads (< 4096 x 1024 trees) are latency-bound: there the floor
     // drops so that every warp of a 4096-warp grid gets about one task (a
@@ -331,6 +368,10 @@ static rt_status plan_launch(rt_handle* h, KernelFn fn, int smem, int64_t n_poin
     const int64_t floor_T = std::min<int64_t>(
         1024, std::max<int64_t>(128, (total / 4096 + 31) / 32 * 32));
     T = total / (int64_t(4096) * 16);
+    if (total >= int64_t(4096) * 1024) {
+      const double tb = std::sqrt(0.6 * static_cast<double>(total) / expected_particles(h, t));
+      T = std::max<int64_t>(T, (static_cast<int64_t>(tb) + 31) / 32 * 32);
+    }
     T = std::max<int64_t>(T, floor_T);
     T = std::min<int64_t>(T, 32768);
   }
@@ -719,7 +760,7 @@ static rt_status run_walk(rt_handle* h, const double* d_points, int64_t n_points
     RT_CUDA(cudaFuncSetAttribute((const void*)prod, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   }
   Launch L;
-  rt_status s = plan_launch(h, prod, smem, n_points, n_trees, L);   // same grid for the trace
+  rt_status s = plan_launch(h, prod, smem, n_points, n_trees, t, L);   // same grid for the trace
   if (s != RT_OK) return s;
   if (sh) return run_walk_shared(h, prod, smem, pool_cap, d_points, n_points, t, tree_offset, n_trees,
                                  seed, rec_shift, d_recs, d_sums, st, L.grid);
